@@ -1,0 +1,371 @@
+"""Benchmark driver (one JSON line on rank 0).
+
+Headline workload (BASELINE.json configs[4], "Minimod 1024^3 grid strong
+scaling 1/2/4/8 GPUs with overlapped halo exchange"): one step = one leapfrog
+time step of the 8th-order acoustic stencil over the whole 1024^3 grid,
+x-slabs of 1024/N planes per GPU, halos stored straight into the neighbours'
+ghost planes by the fused kernel.  metric = Gpts/s (interior points x steps /
+max-over-ranks device time).  Fields are 8.8 GB each at N=1 (always > L2), so
+no L2 flush is needed.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload stencil|p2p|allreduce|dgemm]
+
+N>1 is launched by the driver as torchrun --nproc-per-node N; each rank
+drives LOCAL_RANK's GPU.  --impl reference times the reference's own compiled
+CPU kernel (oracle/_ref, built from reference/pkg/src/diomp/kernels/_core.c)
+on the host cores, same metric and config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+GRID = int(os.environ.get("BENCH_GRID", "1024"))
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def _peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def _traffic_per_launch(key: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
+    ncu --set full capture summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(HERE, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int, interval_ms: int = 50):
+        self.gpu, self.interval = gpu, interval_ms
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", f"-lms", str(self.interval)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())
+                if any(r[3].replace(".", "").isdigit() for r in rows) else None}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / baseline (oracle/_ref = the reference's compiled kernel)
+# ---------------------------------------------------------------------------
+
+_W = {}
+
+
+def _cpu_init(kind, planes, ny, nz):
+    import numpy as np
+    sys.path.insert(0, HERE)
+    from oracle import oracle as O
+    _, w = O.time_params(4)
+    shape = (planes + 8, ny + 8, nz + 8)
+    u_cur = np.full(shape, 0.25)
+    u_cur[1::3] = -0.5
+    _W.update(u_cur=u_cur, u_prev=u_cur * 0.5, w=w, center=3.0 * w[0],
+              pts=planes * ny * nz,
+              fn=_load_ref_core().stencil_update if kind == "reference" else O.stencil_update_c)
+    _cpu_step(0)  # warm
+
+
+def _cpu_step(_):
+    t0 = time.perf_counter()
+    w = _W["w"]
+    _W["fn"](_W["u_prev"], _W["u_cur"], _W["u_prev"], _W["center"], w, w, w, 4)
+    return _W["pts"], time.perf_counter() - t0
+
+
+def _load_ref_core():
+    import importlib.util
+    d = os.path.join(HERE, "oracle", "_ref")
+    for f in sorted(os.listdir(d)):
+        if f.startswith("_core") and f.endswith(".so"):
+            spec = importlib.util.spec_from_file_location("_core", os.path.join(d, f))
+            mod = importlib.util.module_from_spec(spec)
+            spec.loader.exec_module(mod)
+            return mod
+    raise ImportError("oracle/_ref/_core*.so not built")
+
+
+class CpuReference:
+    """The reference's compiled stencil_update (oracle/_ref, built from
+    reference/pkg/src/diomp/kernels/_core.c with -O3 -ffp-contract=off) on
+    the host cores: one x-slab per process, like the reference's
+    one-single-threaded-rank-per-core layout.  kind = "port" when only the
+    oracle restatement is available."""
+
+    def __init__(self, grid: int, planes: int = 8, max_cores: int = 64):
+        import multiprocessing as mp
+        self.kind = "reference"
+        try:
+            _load_ref_core()
+        except Exception:
+            self.kind = "port"
+        self.cores = min(os.cpu_count() or 1, max_cores)
+        self.planes, self.grid = planes, grid
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_cpu_init,
+                                                initargs=(self.kind, planes, grid, grid))
+
+    def step(self) -> float:
+        """One stencil step on every core's slab; aggregate Gpts/s."""
+        res = self.pool.map(_cpu_step, range(self.cores), chunksize=1)
+        return sum(r[0] for r in res) / max(r[1] for r in res) / 1e9
+
+    def describe(self, value: float, steps: int) -> dict:
+        return {"value": round(value, 4), "unit": "Gpts/s", "cores": self.cores, "kind": self.kind,
+                "sample": f"{self.cores} processes x {steps} steps of a "
+                          f"{self.planes}x{self.grid}x{self.grid} slab each (reference "
+                          f"stencil_update, aggregate over cores)"}
+
+    def close(self):
+        self.pool.terminate()
+
+
+def cpu_baseline(grid: int, steps: int = 3) -> dict:
+    ref = CpuReference(grid)
+    try:
+        vals = [ref.step() for _ in range(steps)]
+        return ref.describe(statistics.median(vals), steps)
+    finally:
+        ref.close()
+
+
+def run_reference_arm(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return 0
+    ref = CpuReference(GRID)
+    try:
+        for _ in range(args.warmup):
+            ref.step()
+        t0 = time.perf_counter()
+        vals = [ref.step() for _ in range(args.steps)]
+        wall = time.perf_counter() - t0
+    finally:
+        ref.close()
+    value = statistics.median(vals)
+    line = {"metric": "minimod_gpts_per_s", "value": round(value, 4), "unit": "Gpts/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"minimod_{GRID}^3_strong_scaling", "grid": [GRID] * 3,
+                       "radius": 4},
+            "impl": "reference", "cpu_baseline": ref.describe(value, args.steps),
+            "e2e": {"value": round(value, 4), "unit": "Gpts/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def _make_runtime(world: int, rank: int, local: int, field_bytes: int):
+    from paper_2506_02486_b200 import (AllocatorKind, LaunchConfig, SegmentConfig, runtime)
+    from paper_2506_02486_b200.config import resolve_from_env
+    need = (2 * field_bytes + (64 << 20)) * 4 // 3
+    seg = 1 << max(24, (need - 1).bit_length())
+    os.environ.setdefault("DIOMP_GPUS", str(local))
+    cfg = resolve_from_env(LaunchConfig(nranks=world, segment=SegmentConfig(
+        seg, AllocatorKind.Linear)))
+    return runtime.Runtime(cfg)
+
+
+def _max_over_ranks(rt, value: float) -> float:
+    import pickle
+    got = rt.ctrl.allgather(tuple(range(rt.nranks)), "bench/max", pickle.dumps(value))
+    return max(pickle.loads(b) for _, b in got)
+
+
+def run_stencil_bench(args):
+    import numpy as np
+    import torch
+
+    from paper_2506_02486_b200 import _native
+    from paper_2506_02486_b200.apps.stencil import StencilRunner, StencilSpec
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    nxl = GRID // world
+    shape = (nxl + 8, GRID + 8, GRID + 8)
+    field_bytes = int(np.prod(shape)) * 8
+    rt = _make_runtime(world, rank, local, field_bytes)
+    spec = StencilSpec(GRID, GRID, GRID, steps=args.steps)
+    runner = StencilRunner(rt, spec)
+    gpu = runner.gpu
+    stream = runner.stream.handle
+
+    # warm-up (>= 3 steps), then K timed steps bracketed by barrier + sync
+    runner.enqueue(max(args.warmup, 3))
+    runner.stream.synchronize()
+    ev0, ev1 = _native.event_create(gpu), _native.event_create(gpu)
+    rt.barrier(rt.world)
+    _native.call("diomp_device_sync", gpu)
+    with ClockSampler(gpu) as clocks:
+        _native.call("diomp_event_record", ev0, stream)
+        runner.enqueue(args.steps)
+        _native.call("diomp_event_record", ev1, stream)
+        _native.call("diomp_event_sync", ev1)
+    _native.check_device(gpu, "stencil bench")
+    rt.barrier(rt.world)
+    ms = _native.event_elapsed_ms(ev0, ev1)
+    ms_max = _max_over_ranks(rt, ms)
+    pts = float(GRID) ** 3 * args.steps
+    value = pts / (ms_max / 1e3) / 1e9
+
+    # roofline: 24 algorithmic bytes per interior point per step (read u_cur,
+    # read u_prev, write u_next); one kernel launch per step per GPU
+    local_pts = nxl * GRID * GRID
+    per_launch_ms = ms / args.steps
+    achieved = 24.0 * local_pts / (per_launch_ms / 1e3) / 1e9
+    peak, peak_src = _peaks()
+    traffic = _traffic_per_launch(f"stencil_{GRID}_n{world}")
+
+    # end to end through the public driver class: host (pinned) initial fields
+    # H2D, K steps, final interior D2H, all inside the timed region
+    runner.free()
+    e2e = None
+    if not args.no_e2e:
+        e2e = _stencil_e2e(rt, spec, args.steps, field_bytes)
+    clk = clocks.summary()
+    if rank == 0:
+        line = {"metric": "minimod_gpts_per_s", "value": round(value, 3), "unit": "Gpts/s",
+                "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+                "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (zero fields + point source, reference initial condition)",
+                "config": {"workload": f"minimod_{GRID}^3_strong_scaling", "grid": [GRID] * 3,
+                           "radius": 4, "decomposition": f"x-slabs of {nxl} planes",
+                           "mode": runner.mode, "l2": "inputs larger than L2 (no flush)",
+                           "parallelism": f"slab{world}"},
+                "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
+                             "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                             "traffic": traffic, "peak_source": peak_src,
+                             "bytes_per_point": 24, "points_per_launch": local_pts},
+                "e2e": e2e, "gpu_launches": args.steps, "clocks": clk}
+        if world == 1 and not args.no_cpu:
+            try:
+                line["cpu_baseline"] = cpu_baseline(GRID)
+            except Exception as e:  # report, do not fail the GPU number
+                line["cpu_baseline"] = {"error": str(e)[:200]}
+        print(json.dumps(line), flush=True)
+    rt.finalize()
+    return 0
+
+
+def _stencil_e2e(rt, spec, steps, field_bytes):
+    import numpy as np
+    import torch
+
+    from paper_2506_02486_b200 import _native
+    from paper_2506_02486_b200.apps.stencil import StencilRunner
+
+    runner = StencilRunner(rt, spec)
+    host_in = torch.zeros(field_bytes // 8, dtype=torch.float64).pin_memory()
+    host_out = torch.empty(field_bytes // 8, dtype=torch.float64).pin_memory()
+    base = rt.gm.base(0)
+    s = runner.stream.handle
+    rt.barrier(rt.world)
+    t0 = time.perf_counter()
+    for rec in (runner.field_a, runner.field_b):
+        _native.call("diomp_memcpy_async", base + rec.addr.offset, host_in.data_ptr(),
+                     field_bytes, 1, s)
+    runner.enqueue(steps)
+    _native.call("diomp_memcpy_async", host_out.data_ptr(), base + runner.cur_rec.addr.offset,
+                 field_bytes, 2, s)
+    runner.stream.synchronize()
+    rt.barrier(rt.world)
+    dt = _max_over_ranks(rt, time.perf_counter() - t0)
+    runner.free()
+    return {"value": round(float(spec.nx) ** 3 * steps / dt / 1e9, 3), "unit": "Gpts/s",
+            "h2d_bytes_per_step": int(2 * field_bytes * rt.nranks / steps),
+            "d2h_bytes_per_step": int(field_bytes * rt.nranks / steps),
+            "note": "public StencilRunner; initial fields H2D from pinned host, final field D2H"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="stencil")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    if args.workload == "stencil":
+        return run_stencil_bench(args)
+    from paper_2506_02486_b200.apps import bench as appbench
+    return appbench.cli_bench(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

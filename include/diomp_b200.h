@@ -1,0 +1,227 @@
+/*
+ * diomp_b200.h -- C ABI of libdiomp_b200.so, the B200-native data plane of the
+ * DiOMP-Offloading hot path (global memory, one-sided put/get, fence/barrier,
+ * OMPCCL bcast/reduce/allreduce, Minimod stencil, row-stripe DGEMM).
+ *
+ * Conventions
+ *   - Plain integers and pointers only: device addresses are uint64_t (UVA),
+ *     streams/events are opaque pointers (cudaStream_t / cudaEvent_t).
+ *   - Every entry point returns an int status: the reference's wire status
+ *     vocabulary (reference/pkg/src/diomp/wire.py:46-52) extended with host
+ *     allocator outcomes, or DIOMP_CUDA_ERROR_BASE + cudaError_t.
+ *   - Entry points are reentrant on distinct streams (runtime.py put/get may be
+ *     called from any thread).  Heap handles are NOT thread-safe:
+ *     allocation is a single-flow collective in the reference.
+ *
+ * Each function names the reference interface it replaces (file:line, paths
+ * relative to reference/pkg/src/diomp/).
+ */
+#ifndef DIOMP_B200_H
+#define DIOMP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (wire.py:46-52 Status + allocator errors) ------------- */
+#define DIOMP_OK 0
+#define DIOMP_INVALID_ADDRESS 1  /* wire.Status.INVALID_ADDRESS -> errors.InvalidAddress */
+#define DIOMP_BAD_REQUEST 2      /* wire.Status.BAD_REQUEST                            */
+#define DIOMP_INTERNAL 3         /* wire.Status.INTERNAL                               */
+#define DIOMP_PENDING 4          /* event/handle not complete yet (HandleState.Pending) */
+#define DIOMP_OUT_OF_SEGMENT 10  /* errors.OutOfSegment (allocators.py)                */
+#define DIOMP_DOUBLE_FREE 11     /* errors.DoubleFree   (allocators.py)                */
+#define DIOMP_CUDA_ERROR_BASE 100
+
+#define DIOMP_MAX_TEAM 64        /* max endpoints in one team / flag array slots       */
+
+const char *diomp_status_string(int status);
+int diomp_version(void);
+int diomp_device_count(int *count);
+int diomp_device_sync(int device);
+/* Device-side wait timeouts (see diomp_wait) are recorded, not trapped:
+ * returns DIOMP_INTERNAL (and clears it) if any wait on `device` timed out. */
+int diomp_device_error(int device);
+int diomp_set_wait_timeout(int device, double seconds); /* default 30 s */
+
+/* ---- segments: global_memory.py:190-206 (GlobalMemory.__init__ arenas),
+ *      segment_create global_memory.py:391-393.  A segment is one zero-filled
+ *      cudaMalloc per device; peers map it by CUDA IPC (one process per GPU)
+ *      or peer access (one process, several GPUs).                          */
+int diomp_seg_create(int device, uint64_t bytes, uint64_t *base_out);
+int diomp_seg_destroy(int device, uint64_t base);
+int diomp_seg_ipc_export(int device, uint64_t base, uint8_t handle_out[64]);
+int diomp_seg_ipc_import(int device, const uint8_t handle[64], uint64_t *base_out);
+int diomp_seg_ipc_close(int device, uint64_t base);
+int diomp_peer_enable(int device, int peer_device);
+
+/* ---- heaps: allocators.py:36-190 (LinearAllocator, BuddyAllocator,
+ *      ReverseBumpAllocator).  Offsets are bit-identical to the reference.  */
+#define DIOMP_HEAP_LINEAR 0  /* (capacity, alignment)                    allocators.py:36-72   */
+#define DIOMP_HEAP_BUDDY 1   /* (capacity, reserve_from; UINT64_MAX=none) allocators.py:75-150 */
+#define DIOMP_HEAP_REVERSE 2 /* (floor=arg, capacity, alignment)         allocators.py:153-190 */
+int diomp_heap_create(int kind, uint64_t capacity, uint64_t arg, uint64_t alignment,
+                      void **heap_out);
+int diomp_heap_destroy(void *heap);
+int diomp_heap_alloc(void *heap, uint64_t size, uint64_t *offset_out);
+int diomp_heap_free(void *heap, uint64_t offset, uint64_t *size_out);
+int diomp_heap_block_size(void *heap, uint64_t size, uint64_t *block_out);
+/* live map in insertion order (the reference's `live` dict); n_inout = capacity in, count out */
+int diomp_heap_live(void *heap, uint64_t *offsets, uint64_t *sizes, uint64_t *n_inout);
+
+/* ---- streams / events: streams.py:56-121 (Stream), runtime.py:472-484
+ *      (_maybe_stream), runtime.py:535-556 (fence = drain of the ledgers). */
+int diomp_stream_create(int device, void **stream_out);
+int diomp_stream_destroy(void *stream);
+int diomp_stream_sync(void *stream);
+int diomp_event_create(int device, void **event_out);
+int diomp_event_record(void *event, void *stream);
+int diomp_event_query(void *event); /* DIOMP_OK when complete, DIOMP_PENDING otherwise */
+int diomp_event_sync(void *event);
+int diomp_event_destroy(void *event);
+int diomp_event_elapsed_ms(void *start, void *stop, float *ms_out);
+int diomp_stream_wait_event(void *stream, void *event);
+
+/* ---- one-sided data plane: runtime.py:371-470 (put/get) replacing
+ *      transport.py:508-566 (rma_put/rma_get frames).  D2D transfers are an
+ *      SM-issued copy kernel launched on `device` (put: the source's device,
+ *      stores cross NVLink; get: the destination's device, loads cross
+ *      NVLink).  dst/src may be peer-mapped addresses.                       */
+int diomp_copy(int device, uint64_t dst, uint64_t src, uint64_t nbytes, void *stream);
+/* host<->device legs of H2D put / D2H get (TransferKind, global_memory.py:52-70) */
+#define DIOMP_H2D 1
+#define DIOMP_D2H 2
+#define DIOMP_D2D 3
+int diomp_memcpy_async(uint64_t dst, uint64_t src, uint64_t nbytes, int kind, void *stream);
+int diomp_memset_async(uint64_t dst, int value, uint64_t nbytes, void *stream);
+/* blocking copy with `device` current (cell reads/writes, host views) */
+int diomp_memcpy_sync(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int kind);
+
+/* ---- device-side synchronisation (replaces the 2 ms host polling of
+ *      runtime.py:535-556 and the TCP dissemination barrier runtime.py:493-513
+ *      inside hot loops).  Flags are u64 counters in symmetric memory:
+ *      signal = st.release.sys, wait = ld.acquire.sys until >= value.       */
+int diomp_signal(int device, uint64_t flag_addr, uint64_t value, void *stream);
+int diomp_wait(int device, uint64_t flag_addr, uint64_t value, void *stream);
+
+/* A team is a communicator as seen by one launching endpoint
+ * (collectives.py:102-143 Communicator / bootstrap: ring order = members
+ * rotated to the root).  base[p] is position p's segment base as addressable
+ * from `device`; flags of endpoint p live at base[p] + flag_off, slot index =
+ * slot[q] (the global endpoint index of the signalling position q).
+ * epoch_to[q] / epoch_from[q]: signals already sent to / received from q on
+ * this pair; an entry+exit synchronised call consumes two (+1 entry, +2 exit)
+ * and the caller advances both by 2 afterwards.  sync=0 skips all flag
+ * traffic (the caller orders the endpoints with host barriers; used when
+ * several endpoints share one GPU).                                           */
+typedef struct {
+    int32_t k;
+    int32_t pos;
+    int32_t device;
+    int32_t sync;
+    uint64_t flag_off;
+    uint64_t counter_off; /* u32 scratch in own segment for last-CTA detection */
+    uint64_t base[DIOMP_MAX_TEAM];
+    uint32_t slot[DIOMP_MAX_TEAM];
+    uint64_t epoch_to[DIOMP_MAX_TEAM];
+    uint64_t epoch_from[DIOMP_MAX_TEAM];
+} diomp_team;
+
+int diomp_team_barrier(const diomp_team *team, void *stream);
+
+/* ---- OMPCCL collectives (collectives.py:232-405).  Offsets are symmetric
+ *      (same on every position).  Results are bit-identical to the
+ *      reference's ring folds:
+ *        reduce:    root gets ((v_root op v_root+1) op ...) op v_root-1
+ *        allreduce: block b=[b*count/k,(b+1)*count/k) folded from position b. */
+#define DIOMP_F32 0
+#define DIOMP_F64 1
+#define DIOMP_I32 2
+#define DIOMP_I64 3
+#define DIOMP_SUM 0
+#define DIOMP_MIN 1
+#define DIOMP_MAX 2
+int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_t root,
+                void *stream);
+int diomp_reduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
+                 int32_t dtype, int32_t op, int32_t root, void *stream);
+int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off,
+                    uint64_t count, int32_t dtype, int32_t op, void *stream);
+
+/* ---- Minimod stencil: kernels/__init__.py:30 seam `stencil_update`
+ *      (reference.py:14-31 / _core.pyx:9-32).  One interior update of
+ *      (NX, NY, NZ) C-order f64 arrays, ghost width `radius` (<= 8); u_next may
+ *      alias u_prev.  Bit-identical to the reference (no FMA, fixed order).  */
+typedef struct {
+    uint64_t u_next, u_cur, u_prev;
+    int64_t NX, NY, NZ;
+    int32_t radius;
+    int32_t _pad;
+    double center;
+    double wx[9], wy[9], wz[9];
+} diomp_stencil_args;
+int diomp_stencil_update(int device, const diomp_stencil_args *args, void *stream);
+
+/* Fused driver step (apps/stencil.py:113-126 + apps/halo_onesided.py:12-25):
+ * update + point source + halo planes stored straight into the neighbours'
+ * ghost planes + per-step neighbour flags.  field[0]/field[1] are the two
+ * local buffers (field_a / field_b of stencil.py:85-86); left/right are the
+ * neighbours' same buffers as addressable from `device` (0 = no neighbour).
+ * Step s uses prev=field[s%2], cur=field[(s+1)%2].                            */
+typedef struct {
+    int32_t device;
+    int32_t radius;       /* must be 4 */
+    int64_t NX, NY, NZ;   /* local extents incl. ghosts: NX = nxl + 2R */
+    uint64_t field[2];
+    uint64_t left_field[2];
+    uint64_t right_field[2];
+    int64_t src_i, src_j, src_k; /* local index of the point source, src_i < 0: none */
+    double amp;
+    double center;
+    double w[5];
+    /* device sync (sync != 0): wait own flag slots, signal neighbours' slots */
+    int32_t sync;
+    int32_t _pad;
+    uint64_t wait_left, wait_right;     /* own flag addresses written by the neighbours */
+    uint64_t sig_left, sig_right;       /* neighbours' flag addresses I write            */
+    uint64_t from_left, from_right;     /* signals already received per neighbour         */
+    uint64_t to_left, to_right;         /* signals already sent per neighbour             */
+    uint64_t counter;                   /* u32 in own segment (last-CTA detection)        */
+} diomp_stencil_plan;
+/* Launch steps [step0, step0+nsteps) on `stream`; each step signals both
+ * neighbours once (caller advances the from/to counters by nsteps).        */
+int diomp_stencil_run(const diomp_stencil_plan *plan, int64_t step0, int64_t nsteps,
+                      void *stream);
+
+/* ---- matmul: kernels/__init__.py:31 seam `matmul_f64` (_core.pyx:35-46):
+ *      c = a @ b with a k-ordered left fold per element, no FMA (bit-exact). */
+int diomp_matmul_f64(int device, int64_t n, int64_t k, int64_t m, uint64_t a, uint64_t b,
+                     uint64_t c, void *stream);
+
+/* Row-stripe ring DGEMM step (apps/cannon.py:119-145): C += A_blk @ B on the
+ * FP64 tensor cores (DMMA), row-major, FMA accumulation (tolerance, not
+ * bit-pinned -- the reference uses BLAS here).  fwd != 0: the kernel also
+ * stores every B element exactly once to fwd (the predecessor's spare stripe,
+ * peer-mapped), fusing the stripe shift of cannon.py:124-131 into the GEMM.
+ * Optional device sync as in the stencil plan (wait on own flags before
+ * reading B / writing fwd, last CTA signals).                                */
+typedef struct {
+    int32_t device;
+    int32_t sync;
+    int64_t M, N, K;
+    uint64_t A, B, C, fwd;
+    int64_t lda, ldb, ldc, ldf;
+    uint64_t wait_addr[2];
+    uint64_t wait_value[2];
+    uint64_t sig_addr[2];
+    uint64_t sig_value[2];
+    uint64_t counter;
+} diomp_dgemm_args;
+int diomp_dgemm(const diomp_dgemm_args *args, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIOMP_B200_H */

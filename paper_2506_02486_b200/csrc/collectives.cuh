@@ -1,0 +1,332 @@
+// OMPCCL collectives over NVLink peer memory (sm_100a).
+//
+// Reference: collectives.py:232-405.  The reference moves 1 MiB chunks around
+// a ring through scratch slots with token flags (collectives.py:146-215); here
+// every position reads/writes its peers' symmetric buffers directly, one
+// kernel per position, so the wire pattern becomes:
+//   allreduce  position p folds block p = [p*count/k, (p+1)*count/k) by loading
+//              it from every position in ring order p, p+1, ... (exactly the
+//              reference's reduce-scatter fold, collectives.py:22-24, 361-382)
+//              and stores the result into every position's recv buffer (the
+//              all-gather, collectives.py:386-405).  Per direction each GPU
+//              moves 2(k-1)/k of the buffer -- the ring's optimum.
+//   reduce     same block split, fold order starting at the root
+//              (collectives.py:19-21, 270-323); results go to the root only.
+//   bcast      the buffer is cut into k-1 blocks, one per non-root position;
+//              each pulls its block from the root and pushes it to the other
+//              non-roots.  The root's egress is exactly one buffer and every
+//              non-root receives exactly one buffer.
+// Entry / exit synchronisation is device-side (system-scope flags, see
+// diomp_team) so back-to-back collectives never race on buffers -- the
+// cross-collective slot race of the reference cannot occur.
+#pragma once
+
+#include "common.cuh"
+
+namespace diomp {
+namespace coll {
+
+constexpr int THREADS = 512;
+
+template <typename T>
+struct Sum {
+    __device__ __forceinline__ static T apply(T a, T b) { return a + b; }
+};
+template <>
+struct Sum<float> {
+    __device__ __forceinline__ static float apply(float a, float b) { return __fadd_rn(a, b); }
+};
+template <>
+struct Sum<double> {
+    __device__ __forceinline__ static double apply(double a, double b) { return __dadd_rn(a, b); }
+};
+template <>
+struct Sum<int32_t> {  // numpy wraps on overflow
+    __device__ __forceinline__ static int32_t apply(int32_t a, int32_t b) {
+        return (int32_t)((uint32_t)a + (uint32_t)b);
+    }
+};
+template <>
+struct Sum<int64_t> {
+    __device__ __forceinline__ static int64_t apply(int64_t a, int64_t b) {
+        return (int64_t)((uint64_t)a + (uint64_t)b);
+    }
+};
+
+// numpy.minimum / numpy.maximum: NaN in either operand propagates (the first
+// if both), otherwise the second operand wins ties (so min(0.0, -0.0) = -0.0).
+template <typename T>
+__device__ __forceinline__ bool isnan_t(T v) { return v != v; }
+
+template <typename T>
+struct Min {
+    __device__ __forceinline__ static T apply(T a, T b) { return (a < b || isnan_t(a)) ? a : b; }
+};
+template <typename T>
+struct Max {
+    __device__ __forceinline__ static T apply(T a, T b) { return (a > b || isnan_t(a)) ? a : b; }
+};
+
+struct Args {
+    diomp_team t;
+    uint64_t send_off, recv_off;
+    uint64_t count;   // elements (bytes for bcast)
+    int32_t root;
+    int32_t mode;     // 0 allreduce, 1 reduce
+};
+
+__device__ __forceinline__ void entry_barrier(const diomp_team &t) {
+    if (!t.sync) return;
+    const int q = threadIdx.x;
+    if (q < t.k && q != t.pos) {
+        if (blockIdx.x == 0) {
+            __threadfence_system();
+            st_release_sys((uint64_t *)(t.base[q] + t.flag_off) + t.slot[t.pos], t.epoch_to[q] + 1);
+        }
+        wait_ge((const uint64_t *)(t.base[t.pos] + t.flag_off) + t.slot[q], t.epoch_from[q] + 1);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void exit_barrier(const diomp_team &t) {
+    if (!t.sync) return;
+    if (last_cta_done((unsigned int *)(t.base[t.pos] + t.counter_off), gridDim.x)) {
+        const int q = threadIdx.x;
+        if (q < t.k && q != t.pos) {
+            st_release_sys((uint64_t *)(t.base[q] + t.flag_off) + t.slot[t.pos], t.epoch_to[q] + 2);
+            wait_ge((const uint64_t *)(t.base[t.pos] + t.flag_off) + t.slot[q], t.epoch_from[q] + 2);
+        }
+    }
+}
+
+// Fold element range [lo, hi) of T over positions start, start+1, ... (mod k)
+// and store to the recv buffer of every position in [dst_lo, dst_hi) (all) or
+// to `only` (reduce).  Vectorised 16 B where the offsets allow.
+template <typename T, typename OP, int KMAX>
+__device__ __forceinline__ void fold_range(const Args &a, uint64_t lo, uint64_t hi, int start,
+                                           int only) {
+    const diomp_team &t = a.t;
+    const int k = t.k;
+    constexpr int V = 16 / sizeof(T);
+    const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gsz = (uint64_t)gridDim.x * blockDim.x;
+    // vector-aligned interior when send/recv offsets share alignment mod 16
+    uint64_t vlo = hi, vhi = hi;
+    if (((a.send_off - a.recv_off) & 15) == 0) {
+        uint64_t first = lo;
+        while (first < hi && ((a.send_off + first * sizeof(T)) & 15)) ++first;
+        vlo = first;
+        vhi = vlo + (hi - vlo) / V * V;
+    }
+    auto src = [&](int p) { return (const T *)(t.base[p] + a.send_off); };
+    auto dst = [&](int p) { return (T *)(t.base[p] + a.recv_off); };
+    // vector body
+    using VT = uint4;
+    for (uint64_t v = vlo / V + gtid; v < vhi / V; v += gsz) {
+        VT buf[KMAX];
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i)
+            if (i < k) {
+                int pidx = start + i;
+                if (pidx >= k) pidx -= k;
+                buf[i] = reinterpret_cast<const VT *>(src(pidx))[v];
+            }
+        T acc[V];
+        const T *b0 = reinterpret_cast<const T *>(&buf[0]);
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = b0[e];
+#pragma unroll
+        for (int i = 1; i < KMAX; ++i)
+            if (i < k) {
+                const T *bi = reinterpret_cast<const T *>(&buf[i]);
+#pragma unroll
+                for (int e = 0; e < V; ++e) acc[e] = OP::apply(acc[e], bi[e]);
+            }
+        VT out = *reinterpret_cast<VT *>(acc);
+        if (only >= 0) {
+            reinterpret_cast<VT *>(dst(only))[v] = out;
+        } else {
+            for (int i = 0; i < k; ++i) {
+                int pidx = t.pos + i;  // own copy first, then peers
+                if (pidx >= k) pidx -= k;
+                reinterpret_cast<VT *>(dst(pidx))[v] = out;
+            }
+        }
+    }
+    // scalar head / tail (and everything when not vectorisable)
+    const uint64_t nhead = vlo - lo, ntail = hi - vhi;
+    for (uint64_t j = gtid; j < nhead + ntail; j += gsz) {
+        const uint64_t e = j < nhead ? lo + j : vhi + (j - nhead);
+        T acc = src(start)[e];
+        for (int i = 1; i < k; ++i) {
+            int pidx = start + i;
+            if (pidx >= k) pidx -= k;
+            acc = OP::apply(acc, src(pidx)[e]);
+        }
+        if (only >= 0) dst(only)[e] = acc;
+        else
+            for (int i = 0; i < k; ++i) dst(i)[e] = acc;
+    }
+}
+
+template <typename T, typename OP, int KMAX>
+__global__ void __launch_bounds__(THREADS) reduce_kernel(const __grid_constant__ Args a) {
+    entry_barrier(a.t);
+    const int k = a.t.k, p = a.t.pos;
+    const uint64_t lo = (uint64_t)p * a.count / k, hi = (uint64_t)(p + 1) * a.count / k;
+    if (a.mode == 0) fold_range<T, OP, KMAX>(a, lo, hi, p, -1);
+    else fold_range<T, OP, KMAX>(a, lo, hi, a.root, a.root);
+    exit_barrier(a.t);
+}
+
+// bcast: non-root position p handles block j = (p - root - 1 mod k) of k-1.
+__global__ void __launch_bounds__(THREADS) bcast_kernel(const __grid_constant__ Args a) {
+    entry_barrier(a.t);
+    const diomp_team &t = a.t;
+    const int k = t.k, p = t.pos, root = a.root;
+    if (p != root) {
+        const uint64_t off = a.send_off, n = a.count;
+        const uint64_t al = (off + 15) & ~(uint64_t)15;
+        const uint64_t body_lo = al - off < n ? al - off : n;
+        const uint64_t nvec = (n - body_lo) / 16;
+        const uint64_t body_hi = body_lo + nvec * 16;
+        int j = p - root - 1;
+        if (j < 0) j += k;
+        const uint64_t vlo = (uint64_t)j * nvec / (k - 1), vhi = (uint64_t)(j + 1) * nvec / (k - 1);
+        const uint4 *src = reinterpret_cast<const uint4 *>(t.base[root] + off + body_lo);
+        const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const uint64_t gsz = (uint64_t)gridDim.x * blockDim.x;
+        constexpr int U = 4;
+        uint64_t v = vlo + gtid;
+        for (; v + (U - 1) * gsz < vhi; v += U * gsz) {
+            uint4 b[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) b[u] = src[v + u * gsz];
+            for (int i = 0; i < k; ++i) {
+                int q = p + i;
+                if (q >= k) q -= k;
+                if (q == root) continue;
+                uint4 *d = reinterpret_cast<uint4 *>(t.base[q] + off + body_lo);
+#pragma unroll
+                for (int u = 0; u < U; ++u) d[v + u * gsz] = b[u];
+            }
+        }
+        for (; v < vhi; v += gsz) {
+            uint4 b = src[v];
+            for (int q = 0; q < k; ++q)
+                if (q != root) reinterpret_cast<uint4 *>(t.base[q] + off + body_lo)[v] = b;
+        }
+        // unaligned head/tail bytes: handled by block-0 owner
+        if (j == 0) {
+            const uint8_t *s8 = reinterpret_cast<const uint8_t *>(t.base[root] + off);
+            const uint64_t ntail = n - body_hi;
+            for (uint64_t i = gtid; i < body_lo + ntail; i += gsz) {
+                const uint64_t e = i < body_lo ? i : body_hi + (i - body_lo);
+                const uint8_t b = s8[e];
+                for (int q = 0; q < k; ++q)
+                    if (q != root) reinterpret_cast<uint8_t *>(t.base[q] + off)[e] = b;
+            }
+        }
+    }
+    exit_barrier(a.t);
+}
+
+static int grid_for(uint64_t work_items) {
+    int64_t want = ceil_div((int64_t)work_items, THREADS);
+    if (want < 1) want = 1;
+    if (want > kNumSMs * 4) want = kNumSMs * 4;
+    return (int)want;
+}
+
+template <typename T, typename OP>
+static int launch_reduce(const Args &a, cudaStream_t s) {
+    const uint64_t per = a.count / a.t.k + 1;
+    const uint64_t items = per / (16 / sizeof(T)) + 1;
+    const int g = grid_for(items);
+    if (a.t.k <= 8) reduce_kernel<T, OP, 8><<<g, THREADS, 0, s>>>(a);
+    else if (a.t.k <= 16) reduce_kernel<T, OP, 16><<<g, THREADS, 0, s>>>(a);
+    else reduce_kernel<T, OP, DIOMP_MAX_TEAM><<<g, THREADS, 0, s>>>(a);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+template <typename T>
+static int dispatch_op(const Args &a, int op, cudaStream_t s) {
+    switch (op) {
+        case DIOMP_SUM: return launch_reduce<T, Sum<T>>(a, s);
+        case DIOMP_MIN: return launch_reduce<T, Min<T>>(a, s);
+        case DIOMP_MAX: return launch_reduce<T, Max<T>>(a, s);
+        default: return DIOMP_BAD_REQUEST;
+    }
+}
+
+static int dispatch(const Args &a, int dtype, int op, cudaStream_t s) {
+    switch (dtype) {
+        case DIOMP_F32: return dispatch_op<float>(a, op, s);
+        case DIOMP_F64: return dispatch_op<double>(a, op, s);
+        case DIOMP_I32: return dispatch_op<int32_t>(a, op, s);
+        case DIOMP_I64: return dispatch_op<int64_t>(a, op, s);
+        default: return DIOMP_BAD_REQUEST;
+    }
+}
+
+static bool team_ok(const diomp_team *t) {
+    return t->k >= 1 && t->k <= DIOMP_MAX_TEAM && t->pos >= 0 && t->pos < t->k;
+}
+
+}  // namespace coll
+}  // namespace diomp
+
+extern "C" {
+
+int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
+                    int32_t dtype, int32_t op, void *stream) {
+    using namespace diomp::coll;
+    if (!team_ok(team)) return DIOMP_BAD_REQUEST;
+    if (count == 0) return DIOMP_OK;
+    DIOMP_CUDA_TRY(cudaSetDevice(team->device));
+    Args a{};
+    a.t = *team;
+    a.send_off = send_off;
+    a.recv_off = recv_off;
+    a.count = count;
+    a.mode = 0;
+    return dispatch(a, dtype, op, (cudaStream_t)stream);
+}
+
+int diomp_reduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
+                 int32_t dtype, int32_t op, int32_t root, void *stream) {
+    using namespace diomp::coll;
+    if (!team_ok(team) || root < 0 || root >= team->k) return DIOMP_BAD_REQUEST;
+    if (count == 0) return DIOMP_OK;
+    DIOMP_CUDA_TRY(cudaSetDevice(team->device));
+    Args a{};
+    a.t = *team;
+    a.send_off = send_off;
+    a.recv_off = recv_off;
+    a.count = count;
+    a.root = root;
+    a.mode = 1;
+    return dispatch(a, dtype, op, (cudaStream_t)stream);
+}
+
+int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_t root, void *stream) {
+    using namespace diomp;
+    using namespace diomp::coll;
+    if (!team_ok(team) || root < 0 || root >= team->k) return DIOMP_BAD_REQUEST;
+    if (nbytes == 0 || team->k == 1) return DIOMP_OK;
+    DIOMP_CUDA_TRY(cudaSetDevice(team->device));
+    Args a{};
+    a.t = *team;
+    a.send_off = offset;
+    a.recv_off = offset;
+    a.count = nbytes;
+    a.root = root;
+    const uint64_t per = nbytes / (uint64_t)(team->k - 1) / 16 + 1;
+    const int g = grid_for(per);
+    bcast_kernel<<<g, THREADS, 0, (cudaStream_t)stream>>>(a);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+}  // extern "C"

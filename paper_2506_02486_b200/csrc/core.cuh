@@ -1,0 +1,358 @@
+// Segments, IPC, streams/events and the one-sided data plane.
+//
+// Replaces the reference's simulated arenas (global_memory.py:190-206) and
+// frame transport (transport.py:508-566, 830-861): a segment is one
+// cudaMalloc per device, peers reach it through CUDA IPC or peer access, and
+// put/get are SM-issued copy kernels whose loads (get) or stores (put) cross
+// NVLink directly -- no frames, no progress thread.
+#pragma once
+
+#include "common.cuh"
+
+namespace diomp {
+
+// ---------------------------------------------------------------------------
+// copy kernel (put / get)
+// ---------------------------------------------------------------------------
+
+// 16-byte vector body: each thread keeps UNROLL independent 16 B loads in
+// flight before storing, which is what hides the ~2 us NVLink round trip of
+// peer loads (get) and keeps enough posted stores outstanding (put).
+template <int UNROLL>
+__global__ void __launch_bounds__(512) copy16_kernel(uint4 *__restrict__ dst,
+                                                     const uint4 *__restrict__ src,
+                                                     uint64_t n16) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (UNROLL - 1) * stride < n16; i += UNROLL * stride) {
+        uint4 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) v[u] = src[i + u * stride];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) dst[i + u * stride] = v[u];
+    }
+    for (; i < n16; i += stride) dst[i] = src[i];
+}
+
+// Unaligned head/tail bytes (and wholly misaligned pairs): plain byte copy.
+__global__ void copy1_kernel(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src,
+                             uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] = src[i];
+}
+
+__global__ void copy8_kernel(uint64_t *__restrict__ dst, const uint64_t *__restrict__ src,
+                             uint64_t n8) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride)
+        dst[i] = src[i];
+}
+
+static int launch_copy(uint64_t dst, uint64_t src, uint64_t n, cudaStream_t s) {
+    if (n == 0) return DIOMP_OK;
+    if (((dst ^ src) & 15) == 0) {
+        uint64_t head = (16 - (dst & 15)) & 15;
+        if (head > n) head = n;
+        if (head) {
+            copy1_kernel<<<1, 32, 0, s>>>((uint8_t *)dst, (const uint8_t *)src, head);
+            DIOMP_LAUNCH_CHECK();
+        }
+        uint64_t body = (n - head) / 16;
+        if (body) {
+            const int threads = 512;
+            const int unroll = 4;
+            int64_t want = ceil_div((int64_t)body, (int64_t)threads * unroll);
+            int blocks = (int)(want < kNumSMs * 4 ? want : kNumSMs * 4);
+            copy16_kernel<unroll><<<blocks, threads, 0, s>>>((uint4 *)(dst + head),
+                                                             (const uint4 *)(src + head), body);
+            DIOMP_LAUNCH_CHECK();
+        }
+        uint64_t tail = n - head - body * 16;
+        if (tail) {
+            uint64_t off = head + body * 16;
+            copy1_kernel<<<1, 32, 0, s>>>((uint8_t *)(dst + off), (const uint8_t *)(src + off),
+                                          tail);
+            DIOMP_LAUNCH_CHECK();
+        }
+        return DIOMP_OK;
+    }
+    if (((dst | src) & 7) == 0) {
+        uint64_t n8 = n / 8;
+        int64_t want = ceil_div((int64_t)n8, 512);
+        int blocks = (int)(want < kNumSMs * 4 ? want : kNumSMs * 4);
+        if (n8) {
+            copy8_kernel<<<blocks, 512, 0, s>>>((uint64_t *)dst, (const uint64_t *)src, n8);
+            DIOMP_LAUNCH_CHECK();
+        }
+        if (n % 8) {
+            copy1_kernel<<<1, 32, 0, s>>>((uint8_t *)(dst + n8 * 8),
+                                          (const uint8_t *)(src + n8 * 8), n % 8);
+            DIOMP_LAUNCH_CHECK();
+        }
+        return DIOMP_OK;
+    }
+    int64_t want = ceil_div((int64_t)n, 512);
+    int blocks = (int)(want < kNumSMs * 4 ? want : kNumSMs * 4);
+    copy1_kernel<<<blocks, 512, 0, s>>>((uint8_t *)dst, (const uint8_t *)src, n);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// flags
+// ---------------------------------------------------------------------------
+
+__global__ void signal_kernel(uint64_t *flag, uint64_t value) {
+    __threadfence_system();
+    st_release_sys(flag, value);
+}
+
+__global__ void wait_kernel(const uint64_t *flag, uint64_t value) { wait_ge(flag, value); }
+
+// Team barrier: thread q signals position q and waits for q's signal.
+__global__ void team_barrier_kernel(diomp_team t) {
+    int q = threadIdx.x;
+    if (q < t.k && q != t.pos) {
+        __threadfence_system();
+        uint64_t *remote = (uint64_t *)(t.base[q] + t.flag_off) + t.slot[t.pos];
+        st_release_sys(remote, t.epoch_to[q] + 1);
+        const uint64_t *mine = (const uint64_t *)(t.base[t.pos] + t.flag_off) + t.slot[q];
+        wait_ge(mine, t.epoch_from[q] + 1);
+    }
+}
+
+}  // namespace diomp
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace diomp;
+
+extern "C" {
+
+const char *diomp_status_string(int status) {
+    switch (status) {
+        case DIOMP_OK: return "ok";
+        case DIOMP_INVALID_ADDRESS: return "invalid address";
+        case DIOMP_BAD_REQUEST: return "bad request";
+        case DIOMP_INTERNAL: return "internal error (device wait timed out)";
+        case DIOMP_PENDING: return "pending";
+        case DIOMP_OUT_OF_SEGMENT: return "out of segment";
+        case DIOMP_DOUBLE_FREE: return "double free";
+        default: break;
+    }
+    if (status >= DIOMP_CUDA_ERROR_BASE) return cudaGetErrorString((cudaError_t)(status - DIOMP_CUDA_ERROR_BASE));
+    return "unknown status";
+}
+
+int diomp_version(void) { return 10000; }
+
+int diomp_device_count(int *count) {
+    DIOMP_CUDA_TRY(cudaGetDeviceCount(count));
+    return DIOMP_OK;
+}
+
+int diomp_device_sync(int device) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    DIOMP_CUDA_TRY(cudaDeviceSynchronize());
+    return DIOMP_OK;
+}
+
+int diomp_device_error(int device) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    unsigned int err = 0, zero = 0;
+    DIOMP_CUDA_TRY(cudaMemcpyFromSymbol(&err, g_device_error, sizeof(err)));
+    if (err) DIOMP_CUDA_TRY(cudaMemcpyToSymbol(g_device_error, &zero, sizeof(zero)));
+    return err ? (int)err : DIOMP_OK;
+}
+
+int diomp_set_wait_timeout(int device, double seconds) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    unsigned long long ns = (unsigned long long)(seconds * 1e9);
+    DIOMP_CUDA_TRY(cudaMemcpyToSymbol(g_wait_timeout_ns, &ns, sizeof(ns)));
+    return DIOMP_OK;
+}
+
+// ---- segments ------------------------------------------------------------
+
+int diomp_seg_create(int device, uint64_t bytes, uint64_t *base_out) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    void *p = nullptr;
+    DIOMP_CUDA_TRY(cudaMalloc(&p, bytes));
+    cudaError_t e = cudaMemset(p, 0, bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return DIOMP_CUDA_ERROR_BASE + (int)e;
+    }
+    *base_out = (uint64_t)p;
+    return DIOMP_OK;
+}
+
+int diomp_seg_destroy(int device, uint64_t base) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    DIOMP_CUDA_TRY(cudaDeviceSynchronize());
+    DIOMP_CUDA_TRY(cudaFree((void *)base));
+    return DIOMP_OK;
+}
+
+int diomp_seg_ipc_export(int device, uint64_t base, uint8_t handle_out[64]) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    DIOMP_CUDA_TRY(cudaIpcGetMemHandle(&h, (void *)base));
+    memcpy(handle_out, &h, 64);
+    return DIOMP_OK;
+}
+
+int diomp_seg_ipc_import(int device, const uint8_t handle[64], uint64_t *base_out) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    void *p = nullptr;
+    DIOMP_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    *base_out = (uint64_t)p;
+    return DIOMP_OK;
+}
+
+int diomp_seg_ipc_close(int device, uint64_t base) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    DIOMP_CUDA_TRY(cudaIpcCloseMemHandle((void *)base));
+    return DIOMP_OK;
+}
+
+int diomp_peer_enable(int device, int peer_device) {
+    if (device == peer_device) return DIOMP_OK;
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    int can = 0;
+    DIOMP_CUDA_TRY(cudaDeviceCanAccessPeer(&can, device, peer_device));
+    if (!can) return DIOMP_BAD_REQUEST;
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return DIOMP_OK;
+    }
+    DIOMP_CUDA_TRY(e);
+    return DIOMP_OK;
+}
+
+// ---- streams / events -------------------------------------------------------
+
+int diomp_stream_create(int device, void **stream_out) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t s;
+    DIOMP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *stream_out = (void *)s;
+    return DIOMP_OK;
+}
+
+int diomp_stream_destroy(void *stream) {
+    DIOMP_CUDA_TRY(cudaStreamDestroy((cudaStream_t)stream));
+    return DIOMP_OK;
+}
+
+int diomp_stream_sync(void *stream) {
+    DIOMP_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    return DIOMP_OK;
+}
+
+int diomp_event_create(int device, void **event_out) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    cudaEvent_t e;
+    DIOMP_CUDA_TRY(cudaEventCreate(&e));
+    *event_out = (void *)e;
+    return DIOMP_OK;
+}
+
+int diomp_event_record(void *event, void *stream) {
+    DIOMP_CUDA_TRY(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream));
+    return DIOMP_OK;
+}
+
+int diomp_event_query(void *event) {
+    cudaError_t e = cudaEventQuery((cudaEvent_t)event);
+    if (e == cudaSuccess) return DIOMP_OK;
+    if (e == cudaErrorNotReady) {
+        cudaGetLastError();
+        return DIOMP_PENDING;
+    }
+    return DIOMP_CUDA_ERROR_BASE + (int)e;
+}
+
+int diomp_event_sync(void *event) {
+    DIOMP_CUDA_TRY(cudaEventSynchronize((cudaEvent_t)event));
+    return DIOMP_OK;
+}
+
+int diomp_event_destroy(void *event) {
+    DIOMP_CUDA_TRY(cudaEventDestroy((cudaEvent_t)event));
+    return DIOMP_OK;
+}
+
+int diomp_event_elapsed_ms(void *start, void *stop, float *ms_out) {
+    DIOMP_CUDA_TRY(cudaEventElapsedTime(ms_out, (cudaEvent_t)start, (cudaEvent_t)stop));
+    return DIOMP_OK;
+}
+
+int diomp_stream_wait_event(void *stream, void *event) {
+    DIOMP_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)event, 0));
+    return DIOMP_OK;
+}
+
+// ---- data plane ---------------------------------------------------------------
+
+int diomp_copy(int device, uint64_t dst, uint64_t src, uint64_t nbytes, void *stream) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    return launch_copy(dst, src, nbytes, (cudaStream_t)stream);
+}
+
+int diomp_memcpy_async(uint64_t dst, uint64_t src, uint64_t nbytes, int kind, void *stream) {
+    if (nbytes == 0) return DIOMP_OK;
+    cudaMemcpyKind k = kind == DIOMP_H2D   ? cudaMemcpyHostToDevice
+                       : kind == DIOMP_D2H ? cudaMemcpyDeviceToHost
+                                           : cudaMemcpyDeviceToDevice;
+    if (kind != DIOMP_H2D && kind != DIOMP_D2H && kind != DIOMP_D2D) return DIOMP_BAD_REQUEST;
+    DIOMP_CUDA_TRY(cudaMemcpyAsync((void *)dst, (const void *)src, nbytes, k, (cudaStream_t)stream));
+    return DIOMP_OK;
+}
+
+int diomp_memset_async(uint64_t dst, int value, uint64_t nbytes, void *stream) {
+    DIOMP_CUDA_TRY(cudaMemsetAsync((void *)dst, value, nbytes, (cudaStream_t)stream));
+    return DIOMP_OK;
+}
+
+int diomp_memcpy_sync(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int kind) {
+    if (nbytes == 0) return DIOMP_OK;
+    if (kind != DIOMP_H2D && kind != DIOMP_D2H && kind != DIOMP_D2D) return DIOMP_BAD_REQUEST;
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    DIOMP_CUDA_TRY(cudaDeviceSynchronize());
+    DIOMP_CUDA_TRY(cudaMemcpy((void *)dst, (const void *)src, nbytes, cudaMemcpyDefault));
+    return DIOMP_OK;
+}
+
+int diomp_signal(int device, uint64_t flag_addr, uint64_t value, void *stream) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((uint64_t *)flag_addr, value);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+int diomp_wait(int device, uint64_t flag_addr, uint64_t value, void *stream) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((const uint64_t *)flag_addr, value);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+int diomp_team_barrier(const diomp_team *team, void *stream) {
+    if (team->k < 1 || team->k > DIOMP_MAX_TEAM || team->pos < 0 || team->pos >= team->k)
+        return DIOMP_BAD_REQUEST;
+    if (team->k == 1 || !team->sync) return DIOMP_OK;
+    DIOMP_CUDA_TRY(cudaSetDevice(team->device));
+    team_barrier_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(*team);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+}  // extern "C"

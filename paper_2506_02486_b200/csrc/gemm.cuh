@@ -1,0 +1,294 @@
+// FP64 matrix multiply (sm_100a).
+//
+// 1. diomp_matmul_f64 -- the kernel seam of kernels/__init__.py:31
+//    (_core.pyx:35-46): c = a @ b with each element a left fold over k in
+//    ascending order, multiplies and adds separately rounded (no FMA), so the
+//    result is bit-identical to the reference oracle.  Register-blocked 4x4
+//    per thread, 64x64 tiles, operands staged through shared memory.
+//
+// 2. diomp_dgemm -- the Cannon block product of apps/cannon.py:138
+//    (C += A_blk @ B_s, BLAS in the reference, tolerance-checked).  tcgen05
+//    has no f64 kind, so the FP64 tensor path on Blackwell is DMMA
+//    (mma.sync.m8n8k4.f64).  128x128x16 CTA tiles, 8 warps of 64x32, 4-stage
+//    cp.async pipeline into bank-conflict-free padded tiles.  When `fwd` is
+//    set, every B tile is additionally stored once to the predecessor's spare
+//    stripe over NVLink straight from shared memory (CTA row mi forwards the
+//    k-tiles kt with kt % n_mtiles == mi), fusing the ring shift of
+//    cannon.py:124-131 into the product.
+#pragma once
+
+#include "common.cuh"
+
+namespace diomp {
+namespace gemm {
+
+// ---------------------------------------------------------------------------
+// exact k-ordered matmul
+// ---------------------------------------------------------------------------
+constexpr int XT = 64;  // output tile
+constexpr int XK = 16;  // k tile
+
+__global__ void __launch_bounds__(256) matmul_exact_kernel(int64_t n, int64_t kk, int64_t m,
+                                                           const double *__restrict__ a,
+                                                           const double *__restrict__ b,
+                                                           double *__restrict__ c) {
+    __shared__ double As[XK][XT + 1];
+    __shared__ double Bs[XK][XT + 1];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int64_t i0 = (int64_t)blockIdx.y * XT, j0 = (int64_t)blockIdx.x * XT;
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) acc[r][s] = 0.0;
+    for (int64_t k0 = 0; k0 < kk; k0 += XK) {
+        for (int e = threadIdx.x; e < XT * XK; e += 256) {
+            const int mi = e / XK, ki = e % XK;  // A: row mi, col ki
+            const int64_t gi = i0 + mi, gk = k0 + ki;
+            As[ki][mi] = (gi < n && gk < kk) ? a[gi * kk + gk] : 0.0;
+            const int kb = e / XT, nj = e % XT;  // B: row kb, col nj
+            const int64_t gkb = k0 + kb, gj = j0 + nj;
+            Bs[kb][nj] = (gkb < kk && gj < m) ? b[gkb * m + gj] : 0.0;
+        }
+        __syncthreads();
+        const int kmax = (int)((kk - k0) < XK ? (kk - k0) : XK);
+        for (int q = 0; q < kmax; ++q) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) av[r] = As[q][ty + 16 * r];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) bv[s] = Bs[q][tx + 16 * s];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int s = 0; s < 4; ++s) acc[r][s] = __dadd_rn(acc[r][s], __dmul_rn(av[r], bv[s]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int64_t gi = i0 + ty + 16 * r, gj = j0 + tx + 16 * s;
+            if (gi < n && gj < m) c[gi * m + gj] = acc[r][s];
+        }
+}
+
+// ---------------------------------------------------------------------------
+// DMMA DGEMM: C += A @ B
+// ---------------------------------------------------------------------------
+constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int APAD = BK + 4;   // A tile row pitch (doubles): conflict-free fragment loads
+constexpr int BPAD = BN + 4;   // B tile row pitch
+constexpr int STAGES = 4;
+constexpr int GTHREADS = 256;
+constexpr int A_STAGE = BM * APAD;
+constexpr int B_STAGE = BK * BPAD;
+constexpr size_t GEMM_SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+
+struct GemmParams {
+    int64_t M, N, K;
+    const double *A;
+    const double *B;
+    double *C;
+    double *fwd;
+    int64_t lda, ldb, ldc, ldf;
+    int32_t sync;
+    const uint64_t *wait_addr[2];
+    uint64_t wait_value[2];
+    uint64_t *sig_addr[2];
+    uint64_t sig_value[2];
+    unsigned int *counter;
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    const int n = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void load_tiles(const GemmParams &p, double *As, double *Bs, int64_t m0,
+                                           int64_t n0, int64_t k0) {
+    // A: BM x BK = 128 rows x 8 chunks of 16 B; B: BK x BN = 16 rows x 64 chunks
+#pragma unroll
+    for (int it = 0; it < (BM * BK / 2) / GTHREADS; ++it) {
+        const int e = threadIdx.x + it * GTHREADS;
+        const int r = e / (BK / 2), ch = e % (BK / 2);
+        const int64_t gr = m0 + r, gk = k0 + ch * 2;
+        const bool ok = gr < p.M && gk < p.K;
+        cp_async16(As + r * APAD + ch * 2, ok ? (const void *)(p.A + gr * p.lda + gk) : (const void *)p.A, ok);
+    }
+#pragma unroll
+    for (int it = 0; it < (BK * BN / 2) / GTHREADS; ++it) {
+        const int e = threadIdx.x + it * GTHREADS;
+        const int r = e / (BN / 2), ch = e % (BN / 2);
+        const int64_t gk = k0 + r, gn = n0 + ch * 2;
+        const bool ok = gk < p.K && gn < p.N;
+        cp_async16(Bs + r * BPAD + ch * 2, ok ? (const void *)(p.B + gk * p.ldb + gn) : (const void *)p.B, ok);
+    }
+}
+
+__global__ void __launch_bounds__(GTHREADS, 1) dgemm_dmma_kernel(const __grid_constant__ GemmParams p) {
+    extern __shared__ __align__(16) double gsm[];
+    double *As = gsm;
+    double *Bs = gsm + STAGES * A_STAGE;
+
+    // swizzle CTAs in groups of 8 m-tiles for L2 reuse of B
+    const int64_t mtiles = ceil_div(p.M, BM), ntiles = ceil_div(p.N, BN);
+    const int64_t bid = blockIdx.x;
+    const int64_t group = 8;
+    const int64_t per_group = group * ntiles;
+    const int64_t g = bid / per_group;
+    const int64_t first_m = g * group;
+    const int64_t gsize = (mtiles - first_m) < group ? (mtiles - first_m) : group;
+    const int64_t mi = first_m + (bid % per_group) % gsize;
+    const int64_t ni = (bid % per_group) / gsize;
+    const int64_t m0 = mi * BM, n0 = ni * BN;
+
+    if (p.sync) {
+        if (threadIdx.x < 2 && p.wait_addr[threadIdx.x])
+            wait_ge(p.wait_addr[threadIdx.x], p.wait_value[threadIdx.x]);
+        __syncthreads();
+    }
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+    const int gq = lane >> 2, tq = lane & 3;
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int64_t ktiles = ceil_div(p.K, BK);
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ktiles) load_tiles(p, As + s * A_STAGE, Bs + s * B_STAGE, m0, n0, (int64_t)s * BK);
+        cp_async_commit();
+    }
+    for (int64_t kt = 0; kt < ktiles; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        const int st = (int)(kt % STAGES);
+        const double *a_s = As + st * A_STAGE;
+        const double *b_s = Bs + st * B_STAGE;
+        // prefetch tile kt + STAGES - 1 into the slot consumed at kt-1
+        const int64_t nk = kt + STAGES - 1;
+        if (nk < ktiles) {
+            const int ns = (int)(nk % STAGES);
+            load_tiles(p, As + ns * A_STAGE, Bs + ns * B_STAGE, m0, n0, nk * BK);
+        }
+        cp_async_commit();
+        // fused ring shift: forward this B tile once to the predecessor
+        if (p.fwd && (kt % mtiles) == mi) {
+            for (int e = threadIdx.x; e < BK * BN / 2; e += GTHREADS) {
+                const int r = e / (BN / 2), ch = e % (BN / 2);
+                const int64_t gk = kt * BK + r, gn = n0 + ch * 2;
+                if (gk < p.K && gn < p.N)
+                    *reinterpret_cast<double2 *>(p.fwd + gk * p.ldf + gn) =
+                        *reinterpret_cast<const double2 *>(b_s + r * BPAD + ch * 2);
+            }
+        }
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[8], bf[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) af[i] = a_s[(wm + i * 8 + gq) * APAD + kk + tq];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = b_s[(kk + tq) * BPAD + wn + j * 8 + gq];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        }
+    }
+    cp_async_wait<0>();
+
+    // epilogue: C = C + acc (numpy's `C += A_blk @ B` order: product, then add)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t r = m0 + wm + i * 8 + gq;
+            const int64_t cidx = n0 + wn + j * 8 + tq * 2;
+            if (r < p.M && cidx + 1 < p.N) {
+                double2 *cp = reinterpret_cast<double2 *>(p.C + r * p.ldc + cidx);
+                double2 cv = *cp;
+                cv.x = __dadd_rn(cv.x, acc[i][j][0]);
+                cv.y = __dadd_rn(cv.y, acc[i][j][1]);
+                *cp = cv;
+            } else if (r < p.M && cidx < p.N) {
+                p.C[r * p.ldc + cidx] = __dadd_rn(p.C[r * p.ldc + cidx], acc[i][j][0]);
+            }
+        }
+
+    if (p.sync && last_cta_done(p.counter, gridDim.x) && threadIdx.x < 2 && p.sig_addr[threadIdx.x])
+        st_release_sys(p.sig_addr[threadIdx.x], p.sig_value[threadIdx.x]);
+}
+
+}  // namespace gemm
+}  // namespace diomp
+
+extern "C" {
+
+int diomp_matmul_f64(int device, int64_t n, int64_t k, int64_t m, uint64_t a, uint64_t b,
+                     uint64_t c, void *stream) {
+    using namespace diomp;
+    using namespace diomp::gemm;
+    if (n <= 0 || m <= 0) return DIOMP_OK;
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    dim3 grid((unsigned)ceil_div(m, XT), (unsigned)ceil_div(n, XT));
+    matmul_exact_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(n, k, m, (const double *)a,
+                                                                 (const double *)b, (double *)c);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
+    using namespace diomp;
+    using namespace diomp::gemm;
+    if (x->M <= 0 || x->N <= 0) return DIOMP_OK;
+    // 16 B cp.async needs even leading dimensions / K / N and aligned bases
+    if ((x->K & 1) || (x->N & 1) || (x->lda & 1) || (x->ldb & 1) || (x->ldc & 1) ||
+        ((x->A | x->B | x->C | x->fwd) & 15) || (x->fwd && (x->ldf & 1)))
+        return DIOMP_BAD_REQUEST;
+    DIOMP_CUDA_TRY(cudaSetDevice(x->device));
+    static bool attr_set[64] = {false};
+    if (x->device < 64 && !attr_set[x->device]) {
+        DIOMP_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)GEMM_SMEM));
+        attr_set[x->device] = true;
+    }
+    GemmParams p{};
+    p.M = x->M; p.N = x->N; p.K = x->K;
+    p.A = (const double *)x->A; p.B = (const double *)x->B; p.C = (double *)x->C;
+    p.fwd = (double *)x->fwd;
+    p.lda = x->lda; p.ldb = x->ldb; p.ldc = x->ldc; p.ldf = x->ldf;
+    p.sync = x->sync;
+    for (int i = 0; i < 2; ++i) {
+        p.wait_addr[i] = (const uint64_t *)x->wait_addr[i];
+        p.wait_value[i] = x->wait_value[i];
+        p.sig_addr[i] = (uint64_t *)x->sig_addr[i];
+        p.sig_value[i] = x->sig_value[i];
+    }
+    p.counter = (unsigned int *)x->counter;
+    const int64_t tiles = ceil_div(x->M, BM) * ceil_div(x->N, BN);
+    dgemm_dmma_kernel<<<(unsigned)tiles, GTHREADS, GEMM_SMEM, (cudaStream_t)stream>>>(p);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,576 @@
+// Minimod 8th-order acoustic-isotropic stencil (sm_100a).
+//
+// Reference: kernels/reference.py:14-31, kernels/_core.pyx:9-32 (per-point
+// order), apps/stencil.py:113-126 (driver step), apps/halo_onesided.py:12-25
+// (Listing-1 halo).  Arithmetic is bit-identical to the reference: every
+// operation is an explicitly rounded __dmul_rn/__dadd_rn/__dsub_rn in the
+// reference's order (acc = c*u; x taps t=1..4; y taps; z taps;
+// (2u - u_prev) + acc), so no FMA contraction can occur.
+//
+// Fast path (R=4, NZ even, 16 B aligned): each CTA owns a 16(y) x 64(z) column
+// of the domain and streams along x through a chunk of planes.
+//   * u_cur planes (tile + 4-wide y/z halo, 24 x 72 f64) arrive by TMA
+//     (cp.async.bulk.tensor.3d) into an 8-slot shared-memory ring, one
+//     mbarrier per slot, prefetching 3 planes ahead.
+//   * every thread owns 2(y) x 2(z) points and keeps the 9-plane x-window of
+//     each in registers; the plane loop is unrolled 9x so the window rotates
+//     by register renaming.  y/z taps come from the centre plane's slot with
+//     16 B shared loads (conflict-free rows).
+//   * u_prev / u_next are streamed with 16 B coalesced global loads/stores.
+// Fused driver epilogue: output planes [R,2R) / [nxl, nxl+R) are also stored
+// into the left / right neighbour's u_next ghost planes over NVLink (peer
+// pointers), the point source is added in-register (one extra rounded add,
+// exactly like stencil.py:124-125), and with sync on, edge CTAs wait for the
+// neighbours' "previous step done" flag while the last CTA to finish signals
+// both neighbours -- the device-side replacement of fence+barrier.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace diomp {
+namespace stencil {
+
+constexpr int R = 4;
+constexpr int TY = 16;
+constexpr int TZ = 64;
+constexpr int BY = TY + 2 * R;  // 24 rows per slot
+constexpr int BZ = TZ + 2 * R;  // 72 columns per slot
+constexpr int SLOT = BY * BZ;   // doubles per slot
+constexpr int NSLOT = 8;
+constexpr int THREADS = 256;
+constexpr uint32_t SLOT_BYTES = SLOT * 8;
+constexpr size_t SMEM_BYTES = (size_t)NSLOT * SLOT_BYTES + 128;
+
+struct Params {
+    double *u_next;
+    const double *u_prev;
+    int64_t NX, NY, NZ;
+    int32_t ntz, ncols;
+    int32_t chunk, nch;
+    double c0;
+    double wx[R + 1], wy[R + 1], wz[R + 1];
+    // fused driver
+    double *left_next;
+    double *right_next;
+    int64_t nxl;
+    int64_t src_x, src_y, src_z;  // src_x < 0: no source
+    double amp;
+    // device sync
+    int32_t sync;
+    const uint64_t *wait_l;
+    const uint64_t *wait_r;
+    uint64_t wl, wr;
+    uint64_t *sig_l;
+    uint64_t *sig_r;
+    uint64_t sl, sr;
+    unsigned int *counter;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_plane(double *dst, const CUtensorMap *map, int z, int y,
+                                               int x, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(z), "r"(y), "r"(x), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ double2 lds2(const double *p) {
+    return *reinterpret_cast<const double2 *>(p);
+}
+
+__device__ __forceinline__ void store4(double *base, int64_t gi0, int64_t gi1, const double (&out)[4],
+                                       bool yv0, bool yv1, bool zv0, bool zv1) {
+    if (yv0 && zv1) *reinterpret_cast<double2 *>(base + gi0) = make_double2(out[0], out[1]);
+    else if (yv0 && zv0) base[gi0] = out[0];
+    if (yv1 && zv1) *reinterpret_cast<double2 *>(base + gi1) = make_double2(out[2], out[3]);
+    else if (yv1 && zv0) base[gi1] = out[2];
+}
+
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap *map, int z, int y, int x) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map),
+                 "r"(z), "r"(y), "r"(x)
+                 : "memory");
+}
+
+__device__ __forceinline__ double2 ldg2(const double *p) {
+    return __ldg(reinterpret_cast<const double2 *>(p));
+}
+
+__device__ __forceinline__ double tap(double acc, double w, double a, double b) {
+    return __dadd_rn(acc, __dmul_rn(w, __dadd_rn(a, b)));
+}
+
+constexpr int PREV_PF = 6;  // u_prev planes prefetched into L2 ahead of use
+
+// One loaded plane q for the thread's 2x2 points.  J is the register-window
+// rotation: window index t (0..8 = planes q-8..q) lives in bank (J+1+t)%9.
+// Per point the operation order is exactly the reference's; the 4 points are
+// interleaved tap by tap, which keeps only a sliding pair of neighbour rows
+// live (row -t / 1+t of tap t are rows 1-(t+1) / (t+1) of tap t+1).
+template <int J>
+__device__ __forceinline__ void step_plane(const Params &p, const double *__restrict__ sm,
+                                           uint64_t *bars, const CUtensorMap *map,
+                                           const CUtensorMap *pmap, double (&Q)[9][4], int q,
+                                           int L, int64_t xa, int y0, int z0, int ry, int zz,
+                                           bool yv0, bool yv1, bool zv0, bool zv1) {
+    const int s = q % NSLOT;
+    const int64_t o = q - 2 * R;  // output plane index within the chunk
+    const int64_t x = xa + o;
+    const int64_t y = y0 + ry, z = z0 + zz;
+    const int64_t gi0 = (x * p.NY + y) * p.NZ + z;
+    const int64_t gi1 = gi0 + p.NZ;
+    double pv[4] = {0.0, 0.0, 0.0, 0.0};
+    if (o >= 0) {  // u_prev of this output plane (L2-resident thanks to the TMA prefetch)
+        if (yv0 && zv1) { double2 v = ldg2(p.u_prev + gi0); pv[0] = v.x; pv[1] = v.y; }
+        else if (yv0 && zv0) pv[0] = __ldg(p.u_prev + gi0);
+        if (yv1 && zv1) { double2 v = ldg2(p.u_prev + gi1); pv[2] = v.x; pv[3] = v.y; }
+        else if (yv1 && zv0) pv[2] = __ldg(p.u_prev + gi1);
+    }
+    mbar_wait(&bars[s], (uint32_t)((q / NSLOT) & 1));
+    {
+        const double *slot = sm + (size_t)s * SLOT + (R + ry) * BZ + R + zz;
+        double2 a = lds2(slot);
+        double2 b = lds2(slot + BZ);
+        Q[J][0] = a.x; Q[J][1] = a.y; Q[J][2] = b.x; Q[J][3] = b.y;
+    }
+    if (o >= 0) {
+        constexpr int C = (J + 5) % 9;  // centre bank
+        const double *cr = sm + (size_t)((q - R) % NSLOT) * SLOT + (R + ry) * BZ + R + zz;
+        double acc[4];
+#pragma unroll
+        for (int pt = 0; pt < 4; ++pt) acc[pt] = __dmul_rn(p.c0, Q[C][pt]);
+        // x taps from the register window
+#pragma unroll
+        for (int t = 1; t <= R; ++t)
+#pragma unroll
+            for (int pt = 0; pt < 4; ++pt)
+                acc[pt] = tap(acc[pt], p.wx[t], Q[(J + 5 + t) % 9][pt], Q[(J + 5 - t + 9) % 9][pt]);
+        // y taps: row a=0 needs rows +t,-t; row a=1 needs rows 1+t, 1-t
+        {
+            double2 rp0 = make_double2(Q[C][2], Q[C][3]);  // row +1 (own row 1)
+            double2 rm1 = make_double2(Q[C][0], Q[C][1]);  // row 0  (own row 0)
+#pragma unroll
+            for (int t = 1; t <= R; ++t) {
+                const double2 rm0 = lds2(cr - t * BZ);        // row -t
+                const double2 rp1 = lds2(cr + (1 + t) * BZ);  // row 1+t
+                acc[0] = tap(acc[0], p.wy[t], rp0.x, rm0.x);
+                acc[1] = tap(acc[1], p.wy[t], rp0.y, rm0.y);
+                acc[2] = tap(acc[2], p.wy[t], rp1.x, rm1.x);
+                acc[3] = tap(acc[3], p.wy[t], rp1.y, rm1.y);
+                rp0 = rp1;  // row t+1 for a=0 at tap t+1
+                rm1 = rm0;  // row -t = 1-(t+1) for a=1 at tap t+1
+            }
+        }
+        // z taps per row: pairs (-4,-3) (-2,-1) [own 0,1] (2,3) (4,5)
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            const double *rr = cr + a * BZ;
+            const double2 m43 = lds2(rr - 4), m21 = lds2(rr - 2), p23 = lds2(rr + 2), p45 = lds2(rr + 4);
+            const double o0 = Q[C][a * 2], o1 = Q[C][a * 2 + 1];
+            double &c0 = acc[a * 2], &c1 = acc[a * 2 + 1];
+            c0 = tap(c0, p.wz[1], o1, m21.y);    c1 = tap(c1, p.wz[1], p23.x, o0);
+            c0 = tap(c0, p.wz[2], p23.x, m21.x); c1 = tap(c1, p.wz[2], p23.y, m21.y);
+            c0 = tap(c0, p.wz[3], p23.y, m43.y); c1 = tap(c1, p.wz[3], p45.x, m21.x);
+            c0 = tap(c0, p.wz[4], p45.x, m43.x); c1 = tap(c1, p.wz[4], p45.y, m43.y);
+        }
+        double out[4];
+#pragma unroll
+        for (int pt = 0; pt < 4; ++pt) {
+            const double u = Q[C][pt];
+            double r = __dadd_rn(__dsub_rn(__dmul_rn(2.0, u), pv[pt]), acc[pt]);
+            if (p.src_x == x && p.src_y == y + (pt >> 1) && p.src_z == z + (pt & 1))
+                r = __dadd_rn(r, p.amp);
+            out[pt] = r;
+        }
+        // stores: local u_next, plus halo planes into the neighbours' ghosts
+        store4(p.u_next, gi0, gi1, out, yv0, yv1, zv0, zv1);
+        if (p.left_next && x < 2 * R)
+            store4(p.left_next + p.nxl * p.NY * p.NZ, gi0, gi1, out, yv0, yv1, zv0, zv1);
+        if (p.right_next && x >= p.nxl)
+            store4(p.right_next - p.nxl * p.NY * p.NZ, gi0, gi1, out, yv0, yv1, zv0, zv1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // slot of plane q-R is free now: refill it with plane q-R+NSLOT
+        if (q >= R && q - R + NSLOT < L) {
+            const int nq = q - R + NSLOT;
+            const int ns = nq % NSLOT;
+            mbar_expect_tx(&bars[ns], SLOT_BYTES);
+            tma_load_plane((double *)sm + (size_t)ns * SLOT, map, z0 - R, y0 - R,
+                           (int)(xa - R + nq), &bars[ns]);
+        }
+        // warm L2 with the u_prev tile PREV_PF output planes ahead
+        const int64_t po = o + 1 + PREV_PF;
+        if (po >= 0 && po < L - 2 * R) tma_prefetch_l2(pmap, z0, y0, (int)(xa + po));
+    }
+}
+
+__global__ void __launch_bounds__(THREADS, 2)
+    stencil_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap pmap,
+                       const __grid_constant__ Params p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *sm = reinterpret_cast<double *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+    __shared__ __align__(8) uint64_t bars[NSLOT];
+
+    // Unit decode: interior chunks first, the two edge chunks (which wait on
+    // and write to the neighbours) last.
+    int c = blockIdx.x / p.ncols;
+    const int col = blockIdx.x % p.ncols;
+    if (p.nch > 2) c = (c < p.nch - 2) ? c + 1 : (c == p.nch - 2 ? 0 : p.nch - 1);
+    const int ty = col / p.ntz, tz = col % p.ntz;
+    const int y0 = R + ty * TY, z0 = R + tz * TZ;
+    const int64_t xa = R + (int64_t)c * p.chunk;
+    int64_t xb = xa + p.chunk;
+    if (xb > p.NX - R) xb = p.NX - R;
+    const int L = (int)(xb - xa) + 2 * R;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ry = 2 * warp, zz = 2 * lane;
+    const bool yv0 = y0 + ry < p.NY - R, yv1 = y0 + ry + 1 < p.NY - R;
+    const bool zv0 = z0 + zz < p.NZ - R, zv1 = z0 + zz + 1 < p.NZ - R;
+
+    if (threadIdx.x == 0) {
+        if (p.sync) {
+            if (xa < 2 * R && p.wait_l) wait_ge(p.wait_l, p.wl);
+            if (xb > p.NX - 2 * R && p.wait_r) wait_ge(p.wait_r, p.wr);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+#pragma unroll
+        for (int s = 0; s < NSLOT; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < NSLOT && q < L; ++q) {
+            mbar_expect_tx(&bars[q], SLOT_BYTES);
+            tma_load_plane(sm + (size_t)q * SLOT, &map, z0 - R, y0 - R, (int)(xa - R + q), &bars[q]);
+        }
+        for (int po = 0; po <= PREV_PF && po < L - 2 * R; ++po)
+            tma_prefetch_l2(&pmap, z0, y0, (int)(xa + po));
+    }
+
+    double Q[9][4];
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) Q[i][j] = 0.0;
+
+#define DIOMP_STEP(JJ)                                                                          \
+    if (q + JJ < L)                                                                             \
+        step_plane<JJ>(p, sm, bars, &map, &pmap, Q, q + JJ, L, xa, y0, z0, ry, zz, yv0, yv1, zv0, \
+                       zv1);
+    for (int q = 0; q < L; q += 9) {
+        DIOMP_STEP(0) DIOMP_STEP(1) DIOMP_STEP(2) DIOMP_STEP(3) DIOMP_STEP(4)
+        DIOMP_STEP(5) DIOMP_STEP(6) DIOMP_STEP(7) DIOMP_STEP(8)
+    }
+#undef DIOMP_STEP
+
+    if (p.sync && last_cta_done(p.counter, gridDim.x) && threadIdx.x == 0) {
+        if (p.sig_l) st_release_sys(p.sig_l, p.sl);
+        if (p.sig_r) st_release_sys(p.sig_r, p.sr);
+    }
+}
+
+// Generic path: any radius <= 8, any even/odd extents, no alignment needs.
+// One thread per interior point, operands straight from global (L1/L2).
+struct GenericParams {
+    double *u_next;
+    const double *u_cur;
+    const double *u_prev;
+    int64_t NX, NY, NZ;
+    int32_t r;
+    double c0;
+    double wx[9], wy[9], wz[9];
+    int64_t src_x, src_y, src_z;
+    double amp;
+};
+
+__global__ void __launch_bounds__(256) stencil_generic_kernel(const __grid_constant__ GenericParams p) {
+    const int64_t ni = p.NX - 2 * p.r, nj = p.NY - 2 * p.r, nk = p.NZ - 2 * p.r;
+    const int64_t total = ni * nj * nk;
+    const int64_t sy = p.NZ, sx = p.NY * p.NZ;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = idx % nk + p.r;
+        const int64_t j = (idx / nk) % nj + p.r;
+        const int64_t i = idx / (nk * nj) + p.r;
+        const int64_t g = i * sx + j * sy + k;
+        const double u = p.u_cur[g];
+        double acc = __dmul_rn(p.c0, u);
+        for (int t = 1; t <= p.r; ++t)
+            acc = __dadd_rn(acc, __dmul_rn(p.wx[t], __dadd_rn(p.u_cur[g + t * sx], p.u_cur[g - t * sx])));
+        for (int t = 1; t <= p.r; ++t)
+            acc = __dadd_rn(acc, __dmul_rn(p.wy[t], __dadd_rn(p.u_cur[g + t * sy], p.u_cur[g - t * sy])));
+        for (int t = 1; t <= p.r; ++t)
+            acc = __dadd_rn(acc, __dmul_rn(p.wz[t], __dadd_rn(p.u_cur[g + t], p.u_cur[g - t])));
+        double out = __dadd_rn(__dsub_rn(__dmul_rn(2.0, u), p.u_prev[g]), acc);
+        if (i == p.src_x && j == p.src_y && k == p.src_z) out = __dadd_rn(out, p.amp);
+        p.u_next[g] = out;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+    });
+    return fn;
+}
+
+static int make_plane_map(CUtensorMap *map, const double *u, int64_t NX, int64_t NY, int64_t NZ,
+                          bool halo = true) {
+    auto encode = get_encode_fn();
+    if (!encode) return DIOMP_INTERNAL;
+    cuuint64_t dims[3] = {(cuuint64_t)NZ, (cuuint64_t)NY, (cuuint64_t)NX};
+    cuuint64_t strides[2] = {(cuuint64_t)NZ * 8, (cuuint64_t)NY * NZ * 8};
+    cuuint32_t box[3] = {halo ? (cuuint32_t)BZ : (cuuint32_t)TZ, halo ? (cuuint32_t)BY : (cuuint32_t)TY, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)u, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? DIOMP_OK : DIOMP_BAD_REQUEST;
+}
+
+static bool fast_path_ok(uint64_t u_next, uint64_t u_cur, uint64_t u_prev, int64_t NX, int64_t NY,
+                         int64_t NZ, int radius) {
+    if (radius != R) return false;
+    if ((NZ & 1) || NX < 3 * R || NY <= 2 * R || NZ <= 2 * R) return false;
+    if ((u_next | u_cur | u_prev) & 15) return false;
+    if (NX > (1ll << 31) || NY > (1ll << 31) || NZ > (1ll << 31)) return false;
+    return true;
+}
+
+// Chunking along x: pick the chunk count minimising
+// rounds(units over resident CTA slots) x (chunk + warm-up cost).
+static void pick_chunks(int64_t nx_int, int ncols, int *chunk_out, int *nch_out) {
+    const int slots = kNumSMs * 2;
+    const char *env = getenv("DIOMP_STENCIL_CHUNK");
+    if (env && atoi(env) > 0) {
+        int ch = atoi(env);
+        if (ch < 2 * R) ch = 2 * R;
+        *chunk_out = ch;
+        *nch_out = (int)ceil_div(nx_int, ch);
+        return;
+    }
+    double best = 1e300;
+    int best_nch = 1;
+    for (int nch = 1; nch <= 64; ++nch) {
+        int64_t chunk = ceil_div(nx_int, nch);
+        if (nch > 1 && chunk < 2 * R) break;
+        int64_t units = (int64_t)ncols * ceil_div(nx_int, chunk);
+        double rounds = (double)ceil_div(units, slots);
+        double cost = rounds * ((double)chunk + 0.35 * 2 * R);
+        if (cost < best * 0.999) {
+            best = cost;
+            best_nch = nch;
+        }
+    }
+    int64_t chunk = ceil_div(nx_int, best_nch);
+    *chunk_out = (int)chunk;
+    *nch_out = (int)ceil_div(nx_int, chunk);
+}
+
+static int launch_fast(const CUtensorMap &map, const CUtensorMap &pmap, Params &p, cudaStream_t s) {
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_set[dev]) {
+        DIOMP_CUDA_TRY(cudaFuncSetAttribute(stencil_tma_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SMEM_BYTES));
+        attr_set[dev] = true;
+    }
+    const int64_t ny_int = p.NY - 2 * R, nz_int = p.NZ - 2 * R, nx_int = p.NX - 2 * R;
+    const int nty = (int)ceil_div(ny_int, TY);
+    p.ntz = (int)ceil_div(nz_int, TZ);
+    p.ncols = nty * p.ntz;
+    pick_chunks(nx_int, p.ncols, &p.chunk, &p.nch);
+    const int64_t units = (int64_t)p.ncols * p.nch;
+    if (units > 0x7fffffff) return DIOMP_BAD_REQUEST;
+    stencil_tma_kernel<<<(unsigned)units, THREADS, SMEM_BYTES, s>>>(map, pmap, p);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+static int launch_generic(const GenericParams &g, cudaStream_t s) {
+    const int64_t total = (g.NX - 2 * g.r) * (g.NY - 2 * g.r) * (g.NZ - 2 * g.r);
+    if (total <= 0) return DIOMP_OK;
+    int64_t blocks = ceil_div(total, 256);
+    if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+    stencil_generic_kernel<<<(unsigned)blocks, 256, 0, s>>>(g);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+}  // namespace stencil
+}  // namespace diomp
+
+extern "C" {
+
+int diomp_stencil_update(int device, const diomp_stencil_args *a, void *stream) {
+    using namespace diomp::stencil;
+    if (a->radius < 0 || a->radius > 8) return DIOMP_BAD_REQUEST;
+    if (a->NX <= 2 * a->radius || a->NY <= 2 * a->radius || a->NZ <= 2 * a->radius) return DIOMP_OK;
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (fast_path_ok(a->u_next, a->u_cur, a->u_prev, a->NX, a->NY, a->NZ, a->radius) &&
+        !getenv("DIOMP_STENCIL_GENERIC")) {
+        CUtensorMap map, pmap;
+        int rc = make_plane_map(&map, (const double *)a->u_cur, a->NX, a->NY, a->NZ);
+        if (rc == DIOMP_OK)
+            rc = make_plane_map(&pmap, (const double *)a->u_prev, a->NX, a->NY, a->NZ, false);
+        if (rc == DIOMP_OK) {
+            Params p{};
+            p.u_next = (double *)a->u_next;
+            p.u_prev = (const double *)a->u_prev;
+            p.NX = a->NX; p.NY = a->NY; p.NZ = a->NZ;
+            p.c0 = a->center;
+            for (int t = 0; t <= R; ++t) { p.wx[t] = a->wx[t]; p.wy[t] = a->wy[t]; p.wz[t] = a->wz[t]; }
+            p.src_x = -1;
+            return launch_fast(map, pmap, p, s);
+        }
+    }
+    GenericParams g{};
+    g.u_next = (double *)a->u_next;
+    g.u_cur = (const double *)a->u_cur;
+    g.u_prev = (const double *)a->u_prev;
+    g.NX = a->NX; g.NY = a->NY; g.NZ = a->NZ;
+    g.r = a->radius;
+    g.c0 = a->center;
+    for (int t = 0; t <= a->radius; ++t) { g.wx[t] = a->wx[t]; g.wy[t] = a->wy[t]; g.wz[t] = a->wz[t]; }
+    g.src_x = -1;
+    return launch_generic(g, s);
+}
+
+int diomp_stencil_run(const diomp_stencil_plan *pl, int64_t step0, int64_t nsteps, void *stream) {
+    using namespace diomp;
+    using namespace diomp::stencil;
+    if (pl->radius != R) return DIOMP_BAD_REQUEST;
+    DIOMP_CUDA_TRY(cudaSetDevice(pl->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nxl = pl->NX - 2 * R;
+    bool fast = fast_path_ok(pl->field[0], pl->field[1], pl->field[0], pl->NX, pl->NY, pl->NZ, R) &&
+                (pl->left_field[0] | pl->left_field[1] | pl->right_field[0] | pl->right_field[1]) % 16 == 0 &&
+                nxl >= 2 * R && !getenv("DIOMP_STENCIL_GENERIC");
+    CUtensorMap maps[2], pmaps[2];
+    if (fast) {
+        for (int b = 0; b < 2 && fast; ++b)
+            fast = make_plane_map(&maps[b], (const double *)pl->field[b], pl->NX, pl->NY, pl->NZ) == DIOMP_OK &&
+                   make_plane_map(&pmaps[b], (const double *)pl->field[b], pl->NX, pl->NY, pl->NZ, false) == DIOMP_OK;
+    }
+    const int64_t plane = pl->NY * pl->NZ;
+    for (int64_t st = step0; st < step0 + nsteps; ++st) {
+        const int pb = (int)(st & 1), cb = 1 - pb;  // prev = field[s%2], cur = field[(s+1)%2]
+        const int64_t k = st - step0;
+        if (fast) {
+            Params p{};
+            p.u_next = (double *)pl->field[pb];
+            p.u_prev = (const double *)pl->field[pb];
+            p.NX = pl->NX; p.NY = pl->NY; p.NZ = pl->NZ;
+            p.c0 = pl->center;
+            for (int t = 0; t <= R; ++t) p.wx[t] = p.wy[t] = p.wz[t] = pl->w[t];
+            p.left_next = (double *)pl->left_field[pb];
+            p.right_next = (double *)pl->right_field[pb];
+            p.nxl = nxl;
+            p.src_x = pl->src_i; p.src_y = pl->src_j; p.src_z = pl->src_k;
+            p.amp = pl->amp;
+            p.sync = pl->sync;
+            if (pl->sync) {
+                p.wait_l = pl->left_field[pb] ? (const uint64_t *)pl->wait_left : nullptr;
+                p.wait_r = pl->right_field[pb] ? (const uint64_t *)pl->wait_right : nullptr;
+                p.wl = pl->from_left + k;     // left finished step st-1
+                p.wr = pl->from_right + k;
+                p.sig_l = pl->left_field[pb] ? (uint64_t *)pl->sig_left : nullptr;
+                p.sig_r = pl->right_field[pb] ? (uint64_t *)pl->sig_right : nullptr;
+                p.sl = pl->to_left + k + 1;
+                p.sr = pl->to_right + k + 1;
+                p.counter = (unsigned int *)pl->counter;
+            }
+            int rc = launch_fast(maps[cb], pmaps[pb], p, s);
+            if (rc) return rc;
+        } else {
+            // Listing-1 order: halo puts, flag exchange, update (+ source).
+            const uint64_t cur = pl->field[cb];
+            const uint64_t slab = (uint64_t)R * plane * 8;
+            if (pl->left_field[cb]) {
+                int rc = launch_copy(pl->left_field[cb] + (uint64_t)(R + nxl) * plane * 8,
+                                     cur + (uint64_t)R * plane * 8, slab, s);
+                if (rc) return rc;
+            }
+            if (pl->right_field[cb]) {
+                int rc = launch_copy(pl->right_field[cb], cur + (uint64_t)nxl * plane * 8, slab, s);
+                if (rc) return rc;
+            }
+            if (pl->sync) {
+                if (pl->left_field[cb]) {
+                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_left, pl->to_left + k + 1);
+                    wait_kernel<<<1, 1, 0, s>>>((const uint64_t *)pl->wait_left, pl->from_left + k + 1);
+                }
+                if (pl->right_field[cb]) {
+                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_right, pl->to_right + k + 1);
+                    wait_kernel<<<1, 1, 0, s>>>((const uint64_t *)pl->wait_right, pl->from_right + k + 1);
+                }
+                DIOMP_LAUNCH_CHECK();
+            }
+            GenericParams g{};
+            g.u_next = (double *)pl->field[pb];
+            g.u_cur = (const double *)cur;
+            g.u_prev = (const double *)pl->field[pb];
+            g.NX = pl->NX; g.NY = pl->NY; g.NZ = pl->NZ;
+            g.r = R;
+            g.c0 = pl->center;
+            for (int t = 0; t <= R; ++t) g.wx[t] = g.wy[t] = g.wz[t] = pl->w[t];
+            g.src_x = pl->src_i; g.src_y = pl->src_j; g.src_z = pl->src_k;
+            g.amp = pl->amp;
+            int rc = launch_generic(g, s);
+            if (rc) return rc;
+        }
+    }
+    return DIOMP_OK;
+}
+
+}  // extern "C"

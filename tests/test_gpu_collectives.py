@@ -1,0 +1,146 @@
+"""Collectives parity on the GPU: the CUDA kernels against the reference's own
+results (tests/golden/collectives_golden.npz, produced by running the
+reference's bcast/reduce/allreduce) -- bitwise, every dtype x op x k."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, NGPU, need_gpus
+
+pytestmark = pytest.mark.gpu
+MIB = 1 << 20
+DT = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64}
+
+
+def contrib(rank, etype, count, seed):
+    """Same generator as tests/golden/make_golden.py."""
+    rng = np.random.default_rng(seed * 100 + rank)
+    if etype.startswith("f"):
+        v = rng.uniform(-1, 1, count).astype(DT[etype])
+        if count > 8:
+            v[3] = np.nan if rank == 1 else v[3]
+            v[5] = -0.0 if rank % 2 else 0.0
+        return v
+    return rng.integers(-2**30, 2**30, count).astype(DT[etype])
+
+
+G = np.load(os.path.join(GOLDEN, "collectives_golden.npz"))
+KEYS = sorted(G.files)
+
+
+def _write(rt, rec, arr, device=0):
+    rt.gm.view(device, rec.addr.offset, arr.nbytes)[:] = arr.view(np.uint8).tobytes()
+
+
+def _read(rt, rec, dtype, count, device=0):
+    return np.frombuffer(bytes(rt.gm.view(device, rec.addr.offset,
+                                          count * np.dtype(dtype).itemsize)), dtype=dtype)
+
+
+@pytest.mark.parametrize("key", [k for k in KEYS if int(k.split("_")[1]) <= 4]
+                         + [k for k in KEYS if int(k.split("_")[1]) == 8][:12])
+def test_reduce_allreduce_match_reference(key):
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200.emulate import run_emulated
+    which, k, et, kind, count, root, seed = key.split("_")
+    k, count, root, seed = int(k), int(count), int(root), int(seed)
+    op = coll.ReduceOp(coll.ReduceKind(kind), coll.ElementType(et))
+    isz = np.dtype(DT[et]).itemsize
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        send = rt.alloc_symmetric(max(count * isz, 64), 0)
+        recv = rt.alloc_symmetric(max(count * isz, 64), 0)
+        _write(rt, send, contrib(rt.rank, et, count, seed))
+        if which == "allreduce":
+            coll.allreduce(comm, send.addr, recv.addr, count, op)
+        else:
+            coll.reduce(comm, send.addr, recv.addr, count, op, root=root)
+        return _read(rt, recv, DT[et], count).tobytes()
+
+    out = run_emulated(k, fn, segment_bytes=2 * MIB)
+    want = G[key].tobytes()
+    if which == "allreduce":
+        assert all(o == want for o in out)
+    else:
+        assert out[root] == want
+
+
+def test_bcast_root_snapshot_sizes_and_roots():
+    from paper_2506_02486_b200 import GlobalAddress
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200.emulate import run_emulated
+    sizes = [1, 100, 128 * 1024, MIB + 7, 4 * MIB + 13]
+    roots = [0, 3, 1, 2, 1]
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        buf = rt.alloc_symmetric(8 * MIB, 0)
+        out = []
+        for size, root in zip(sizes, roots):
+            mine = np.random.default_rng(1000 + size + rt.rank).integers(0, 256, size,
+                                                                         dtype=np.uint8)
+            rt.gm.view(0, buf.addr.offset + 3, size)[:] = mine.tobytes()
+            coll.bcast(comm, GlobalAddress(rt.rank, 0, buf.addr.offset + 3), size, root=root)
+            out.append((mine.tobytes() if rt.rank == root else None,
+                        bytes(rt.gm.view(0, buf.addr.offset + 3, size))))
+        return out
+
+    res = run_emulated(4, fn, segment_bytes=32 * MIB)
+    for i in range(len(sizes)):
+        snap = next(r[i][0] for r in res if r[i][0] is not None)
+        assert all(r[i][1] == snap for r in res)
+
+
+def test_allreduce_in_place_and_big_count():
+    from oracle import oracle as O
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200.emulate import run_emulated
+    count = 3 * MIB // 8 + 5
+    op = coll.ReduceOp(coll.ReduceKind.Sum, coll.ElementType.f64)
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        buf = rt.alloc_symmetric(count * 8, 0)
+        _write(rt, buf, np.random.default_rng(50 + rt.rank).uniform(-1, 1, count))
+        coll.allreduce(comm, buf.addr, buf.addr, count, op)
+        return _read(rt, buf, np.float64, count).tobytes()
+
+    out = run_emulated(3, fn, segment_bytes=64 * MIB)
+    want = O.allreduce_fold([np.random.default_rng(50 + r).uniform(-1, 1, count)
+                             for r in range(3)], "sum").tobytes()
+    assert all(o == want for o in out)
+
+
+@need_gpus(2)
+def test_device_flag_mode_back_to_back():
+    """Ranks on distinct GPUs: entry/exit flags, many consecutive collectives
+    (the reference deadlocks here without a barrier between reps)."""
+    from oracle import oracle as O
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200.emulate import run_emulated
+    k = min(NGPU, 4)
+    count = 100_003
+    op = coll.ReduceOp(coll.ReduceKind.Sum, coll.ElementType.f32)
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        assert comm.device_sync
+        send = rt.alloc_symmetric(count * 4, 0)
+        recv = rt.alloc_symmetric(count * 4, 0)
+        outs = []
+        for rep in range(20):
+            _write(rt, send, np.random.default_rng(rep * 10 + rt.rank).uniform(-1, 1, count)
+                   .astype(np.float32))
+            coll.allreduce(comm, send.addr, recv.addr, count, op)
+            outs.append(_read(rt, recv, np.float32, count).tobytes())
+            coll.bcast(comm, recv.addr, count * 4, root=rep % k)
+        return outs
+
+    res = run_emulated(k, fn, segment_bytes=8 * MIB)
+    for rep in range(20):
+        want = O.allreduce_fold([np.random.default_rng(rep * 10 + r).uniform(-1, 1, count)
+                                 .astype(np.float32) for r in range(k)], "sum").tobytes()
+        assert all(r[rep] == want for r in res)
