@@ -1,0 +1,348 @@
+"""Micro-benchmarks: point-to-point latency/bandwidth and collective sweeps
+(API of reference/pkg/src/diomp/apps/bench.py:1-174; CSV columns
+kind,size_bytes,iters,mean_us,bw_MiBs unchanged).
+
+Timing is on the device (CUDA events on the RMA stream, max over ranks for
+collectives) unless a row measures host-visible latency (put+fence, get+wait),
+which -- like the reference -- includes the host round trip.  `transfer`
+selects the reference's host-sourced payloads (None: H2D put / D2H get) or
+GPU-resident D2D payloads (the NVLink sweep of BASELINE.json configs[1]).
+"""
+
+from __future__ import annotations
+
+import enum
+import json
+import math
+import os
+import pickle
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .. import _native
+from .. import collectives as coll
+from ..errors import UsageError
+from ..global_memory import GlobalAddress, TransferKind
+from ..runtime import Runtime
+
+CSV_HEADER = "kind,size_bytes,iters,mean_us,bw_MiBs"
+MIB = 1024 * 1024
+NVLINK_PEER_GBS = 770.0      # measured peer copy per direction (B200_PROFILING.md)
+NVLINK_NOMINAL_GBS = 900.0
+
+
+class BenchKind(enum.Enum):
+    PutLatency = "put"
+    GetLatency = "get"
+    Bandwidth = "bw"
+    Bcast = "bcast"
+    Allreduce = "allreduce"
+    GetBandwidth = "get_bw"
+
+
+def latency_sizes() -> list[int]:
+    return [4 << i for i in range(12)]
+
+
+def collective_sizes() -> list[int]:
+    return [(128 * 1024) << i for i in range(10)]
+
+
+@dataclass(frozen=True)
+class BenchSpec:
+    kind: BenchKind
+    sizes: tuple
+    iters: int = 100
+    warmup: int = 5
+    transfer: TransferKind | None = None
+
+    def __post_init__(self):
+        if self.iters < 1:
+            raise UsageError("iters must be >= 1")
+        if list(self.sizes) != sorted(self.sizes):
+            raise UsageError("sizes must be ascending")
+
+
+@dataclass
+class BenchRow:
+    kind: str
+    size_bytes: int
+    iters: int
+    mean_us: float
+    bw_mibs: float
+    wire_put_bytes: int = 0
+    ratio: float | None = None
+
+    def csv(self) -> str:
+        base = f"{self.kind},{self.size_bytes},{self.iters},{self.mean_us:.3f},{self.bw_mibs:.3f}"
+        return base + (f",{self.ratio:.4f}" if self.ratio is not None else "")
+
+
+class _Timer:
+    """CUDA-event timer on the rank's RMA stream of device 0."""
+
+    def __init__(self, rt: Runtime):
+        self.rt = rt
+        self.gpu = rt.gpus[0]
+        self.stream = rt._rma_streams[0].handle
+        self.e0 = _native.event_create(self.gpu)
+        self.e1 = _native.event_create(self.gpu)
+
+    def start(self):
+        _native.call("diomp_event_record", self.e0, self.stream)
+
+    def stop_ms(self) -> float:
+        _native.call("diomp_event_record", self.e1, self.stream)
+        _native.call("diomp_event_sync", self.e1)
+        return _native.event_elapsed_ms(self.e0, self.e1)
+
+
+def run_p2p(rt: Runtime, spec: BenchSpec) -> list[BenchRow]:
+    """Rank 0 drives transfers against rank 1; other ranks cooperate."""
+    if rt.nranks < 2:
+        raise UsageError("p2p benchmark needs at least 2 ranks")
+    size_max = max(spec.sizes)
+    buf = rt.alloc_symmetric(size_max, 0)
+    src = rt.alloc_symmetric(size_max, 0)
+    rows: list[BenchRow] = []
+    rt.barrier(rt.world)
+    if rt.rank == 0:
+        dst = rt.translate(buf.addr, 1)
+        stats = rt.engine.stats
+        timer = _Timer(rt)
+        d2d = spec.transfer is TransferKind.D2D
+        for size in spec.sizes:
+            payload = np.random.default_rng(size).integers(0, 256, size, dtype=np.uint8)
+            sink = bytearray(size)
+            if d2d:
+                rt.gm.view(0, src.addr.offset, size)[:] = payload.tobytes()
+            for _ in range(spec.warmup):
+                _one_rep(rt, spec.kind, dst, payload, sink, size, 1, d2d, src)
+            wire0 = stats.put_bytes_total()
+            t0 = time.perf_counter()
+            if d2d and spec.kind in (BenchKind.Bandwidth, BenchKind.GetBandwidth):
+                timer.start()
+                reps = _one_rep(rt, spec.kind, dst, payload, sink, size, spec.iters, d2d, src,
+                                fence=False)
+                elapsed = timer.stop_ms() / 1e3
+                rt.fence(rt.world)
+            else:
+                reps = _one_rep(rt, spec.kind, dst, payload, sink, size, spec.iters, d2d, src)
+                elapsed = time.perf_counter() - t0
+            wire = stats.put_bytes_total() - wire0
+            rows.append(BenchRow(spec.kind.value + ("_d2d" if d2d else ""), size, reps,
+                                 elapsed / reps * 1e6, size * reps / elapsed / MIB, wire))
+    rt.barrier(rt.world)
+    return rows
+
+
+def _one_rep(rt, kind, dst, payload, sink, size, iters, d2d, src, fence=True) -> int:
+    local = GlobalAddress(rt.rank, 0, src.addr.offset)
+    if kind is BenchKind.PutLatency:
+        for _ in range(iters):
+            if d2d:
+                rt.put(dst, local, size, TransferKind.D2D)
+            else:
+                rt.put(dst, payload, size, TransferKind.H2D)
+            rt.fence(rt.world)
+        return iters
+    if kind is BenchKind.GetLatency:
+        for _ in range(iters):
+            if d2d:
+                rt.get(dst, local, size, TransferKind.D2D).wait(rt.cfg.timeout)
+            else:
+                rt.get(dst, sink, size, TransferKind.D2H).wait(rt.cfg.timeout)
+        return iters
+    if kind in (BenchKind.Bandwidth, BenchKind.GetBandwidth):
+        for _ in range(iters):
+            if kind is BenchKind.GetBandwidth:
+                rt.get(dst, local, size, TransferKind.D2D)
+            elif d2d:
+                rt.put(dst, local, size, TransferKind.D2D)
+            else:
+                rt.put(dst, payload, size, TransferKind.H2D)
+        if fence:
+            rt.fence(rt.world)
+        return iters
+    raise UsageError(f"{kind} is not a point-to-point benchmark")
+
+
+def run_collective(rt: Runtime, spec: BenchSpec, comm=None) -> list[BenchRow]:
+    """Warm-up then `iters` timed repetitions per size (device-timed, max over
+    ranks); rank 0 reports.  No barrier is needed between repetitions."""
+    if spec.kind not in (BenchKind.Bcast, BenchKind.Allreduce):
+        raise UsageError(f"{spec.kind} is not a collective benchmark")
+    if comm is None:
+        comm = coll.bootstrap(rt, rt.world)
+    if comm.size < 2:
+        raise UsageError("collective benchmark needs at least 2 endpoints")
+    max_size = max(spec.sizes)
+    send = rt.alloc_symmetric(max_size, 0)
+    recv = rt.alloc_symmetric(max_size, 0)
+    op = coll.ReduceOp(coll.ReduceKind.Sum, coll.ElementType.f32)
+    vals = np.random.default_rng(1000 + rt.rank).uniform(-1, 1, max_size // 4).astype(np.float32)
+    rt.gm.view(0, send.addr.offset, vals.nbytes)[:] = vals.tobytes()
+    rows: list[BenchRow] = []
+    for size in spec.sizes:
+        def run_once():
+            if spec.kind is BenchKind.Bcast:
+                coll.bcast(comm, send.addr, size, root=0)
+            else:
+                coll.allreduce(comm, send.addr, recv.addr, size // 4, op)
+        for _ in range(spec.warmup):
+            run_once()
+        rt.barrier(rt.world)
+        t0 = time.perf_counter()
+        for _ in range(spec.iters):
+            run_once()
+        elapsed = time.perf_counter() - t0
+        got = rt.ctrl.allgather(tuple(range(rt.nranks)), "collbench", pickle.dumps(elapsed))
+        elapsed = max(pickle.loads(b) for _, b in got)
+        if rt.rank == 0:
+            rows.append(BenchRow(spec.kind.value, size, spec.iters, elapsed / spec.iters * 1e6,
+                                 size * spec.iters / elapsed / MIB))
+    rt.free(recv)
+    rt.free(send)
+    return rows
+
+
+def apply_baseline(rows: list[BenchRow], baseline_csv: str):
+    """ratio = log10(baseline_mean / measured_mean), matched by kind+size."""
+    table = {}
+    for line in baseline_csv.strip().splitlines():
+        if line.startswith("kind,") or not line.strip():
+            continue
+        parts = line.split(",")
+        table[(parts[0], int(parts[1]))] = float(parts[3])
+    for row in rows:
+        base = table.get((row.kind, row.size_bytes))
+        if base is not None and row.mean_us > 0:
+            row.ratio = math.log10(base / row.mean_us)
+
+
+def to_csv(rows: list[BenchRow], with_ratio: bool = False) -> str:
+    header = CSV_HEADER + (",log10_ratio" if with_ratio else "")
+    return "\n".join([header] + [r.csv() for r in rows]) + "\n"
+
+
+# ---------------------------------------------------------------------------
+# bench.py --workload p2p | allreduce | bcast | dgemm  (secondary JSON lines)
+# ---------------------------------------------------------------------------
+
+def _cli_runtime(seg_bytes: int):
+    from ..config import LaunchConfig, resolve_from_env
+    from ..global_memory import AllocatorKind, SegmentConfig
+    from ..runtime import Runtime
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("DIOMP_GPUS", str(local))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg = resolve_from_env(LaunchConfig(nranks=world, segment=SegmentConfig(
+        seg_bytes, AllocatorKind.Linear)))
+    return Runtime(cfg)
+
+
+def _line(rt, metric, value, unit, args, config, extra):
+    d = {"metric": metric, "value": value, "unit": unit, "n_gpus": rt.nranks,
+         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+         "scaling": "weak", "vs_baseline": None, "data": "synthetic", "config": config}
+    d.update(extra)
+    print(json.dumps(d), flush=True)
+
+
+def _p2p_cli(args):
+    rt = _cli_runtime(4 << 30)
+    if rt.nranks < 2:
+        raise UsageError("--workload p2p needs 2 GPUs (torchrun --nproc-per-node 2)")
+    sizes = tuple(8 << i for i in range(28))  # 8 B .. 1 GiB
+    out = {}
+    for kind in (BenchKind.Bandwidth, BenchKind.GetBandwidth, BenchKind.PutLatency,
+                 BenchKind.GetLatency):
+        szs = sizes if kind in (BenchKind.Bandwidth, BenchKind.GetBandwidth) else sizes[:11]
+        rows = run_p2p(rt, BenchSpec(kind, szs, iters=max(args.steps, 5), warmup=args.warmup,
+                                     transfer=TransferKind.D2D))
+        out[kind.value] = [(r.size_bytes, round(r.mean_us, 3),
+                            round(r.size_bytes / r.mean_us / 1e3, 2)) for r in rows]
+    if rt.rank == 0:
+        big = [gbps for n, _, gbps in out["bw"] if n >= 64 * MIB]
+        value = out["bw"][-1][2]
+        _line(rt, "put_bandwidth_1GiB", value, "GB/s", args,
+              {"workload": "p2p_d2d_sweep_8B_1GiB", "pair": "rank0->rank1",
+               "symmetric": True},
+              {"roofline": {"bound": "nvlink", "achieved": value, "peak": NVLINK_PEER_GBS,
+                            "unit": "GB/s", "frac": round(value / NVLINK_PEER_GBS, 4),
+                            "nominal": NVLINK_NOMINAL_GBS},
+               "min_bw_ge_64MiB": min(big) if big else None,
+               "get_bandwidth_1GiB": out["get_bw"][-1][2],
+               "put_latency_us_8B": out["put"][0][1], "get_latency_us_8B": out["get"][0][1],
+               "rows": out, "row_format": "[bytes, mean_us, GB/s]"})
+    rt.finalize()
+    return 0
+
+
+def _coll_cli(args, kind):
+    rt = _cli_runtime(8 << 30)
+    if rt.nranks < 2:
+        raise UsageError(f"--workload {kind} needs >= 2 GPUs")
+    sizes = tuple(1024 << (2 * i) for i in range(11))  # 1 KiB .. 1 GiB (x4)
+    bk = BenchKind.Allreduce if kind == "allreduce" else BenchKind.Bcast
+    rows = run_collective(rt, BenchSpec(bk, sizes, iters=max(args.steps, 3),
+                                        warmup=args.warmup))
+    if rt.rank == 0:
+        k = rt.nranks
+        factor = 2 * (k - 1) / k if kind == "allreduce" else 1.0
+        table = [(r.size_bytes, round(r.mean_us, 2),
+                  round(factor * r.size_bytes / r.mean_us / 1e3, 2)) for r in rows]
+        value = table[-1][2]
+        _line(rt, f"{kind}_busbw_1GiB", value, "GB/s", args,
+              {"workload": f"{kind}_f32_sum_sweep_1KiB_1GiB", "endpoints": k},
+              {"roofline": {"bound": "nvlink", "achieved": value, "peak": NVLINK_PEER_GBS,
+                            "unit": "GB/s", "frac": round(value / NVLINK_PEER_GBS, 4)},
+               "rows": table, "row_format": "[bytes, mean_us, busBW GB/s]"})
+    rt.finalize()
+    return 0
+
+
+def _dgemm_cli(args):
+    from .cannon import CannonRing, MatmulSpec
+    n = int(os.environ.get("BENCH_GEMM_N", "16384"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    stripe = (n // world) * n * 8
+    rt = _cli_runtime(1 << max(30, (4 * stripe + (64 << 20) - 1).bit_length()))
+    spec = MatmulSpec(n, rt.nranks)
+    ring = CannonRing(rt, spec, device_seed=0)
+    timer = _Timer(rt)
+    for _ in range(max(args.warmup, 1)):
+        ring.run()
+    rt.barrier(rt.world)
+    ms = []
+    for _ in range(max(args.steps, 1)):
+        rt.barrier(rt.world)
+        timer.stream = ring._stream(0)
+        timer.start()
+        for _ in range(spec.p):
+            ring.enqueue_step() if ring.sync else ring.run()
+        ms.append(timer.stop_ms())
+        ring.synchronize()
+    got = rt.ctrl.allgather(tuple(range(rt.nranks)), "gemmbench", pickle.dumps(min(ms)))
+    t = max(pickle.loads(b) for _, b in got) / 1e3
+    if rt.rank == 0:
+        tflops = 2.0 * n ** 3 / t / 1e12
+        _line(rt, "dgemm_ring_tflops", round(tflops, 3), "TFLOP/s", args,
+              {"workload": f"cannon_ring_{n}^2_fp64", "endpoints": rt.nranks,
+               "kernel": "DMMA m8n8k4 + fused stripe shift"},
+              {"ms_per_multiply": round(t * 1e3, 3)})
+    ring.release()
+    rt.finalize()
+    return 0
+
+
+def cli_bench(args) -> int:
+    if args.workload == "p2p":
+        return _p2p_cli(args)
+    if args.workload in ("allreduce", "bcast"):
+        return _coll_cli(args, args.workload)
+    if args.workload == "dgemm":
+        return _dgemm_cli(args)
+    raise UsageError(f"unknown workload {args.workload!r}")

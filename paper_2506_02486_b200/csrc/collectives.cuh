@@ -32,13 +32,27 @@ template <typename T>
 struct Sum {
     __device__ __forceinline__ static T apply(T a, T b) { return a + b; }
 };
+// numpy's float add runs on x86 SSE/AVX, whose NaN rules differ from the GPU's
+// canonical NaN: a NaN operand propagates (the first one if both), quieted,
+// and an invalid operation (inf - inf) yields the x86 "default NaN" (sign
+// set).  Reproduce them so NaN payloads are bit-identical to the reference.
 template <>
 struct Sum<float> {
-    __device__ __forceinline__ static float apply(float a, float b) { return __fadd_rn(a, b); }
+    __device__ __forceinline__ static float apply(float a, float b) {
+        if (a != a) return __int_as_float(__float_as_int(a) | 0x00400000);
+        if (b != b) return __int_as_float(__float_as_int(b) | 0x00400000);
+        const float r = __fadd_rn(a, b);
+        return r != r ? __int_as_float((int)0xFFC00000u) : r;
+    }
 };
 template <>
 struct Sum<double> {
-    __device__ __forceinline__ static double apply(double a, double b) { return __dadd_rn(a, b); }
+    __device__ __forceinline__ static double apply(double a, double b) {
+        if (a != a) return __longlong_as_double(__double_as_longlong(a) | 0x0008000000000000ll);
+        if (b != b) return __longlong_as_double(__double_as_longlong(b) | 0x0008000000000000ll);
+        const double r = __dadd_rn(a, b);
+        return r != r ? __longlong_as_double((long long)0xFFF8000000000000ull) : r;
+    }
 };
 template <>
 struct Sum<int32_t> {  // numpy wraps on overflow

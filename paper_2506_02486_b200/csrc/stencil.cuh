@@ -41,10 +41,11 @@ constexpr int TZ = 64;
 constexpr int BY = TY + 2 * R;  // 24 rows per slot
 constexpr int BZ = TZ + 2 * R;  // 72 columns per slot
 constexpr int SLOT = BY * BZ;   // doubles per slot
-constexpr int NSLOT = 8;
-constexpr int THREADS = 256;
+constexpr int NSLOT = 16;                 // plane ring: 5 in use + 11 in flight
+constexpr int NCW = 8;                    // compute warps (2 rows each)
+constexpr int THREADS = (NCW + 1) * 32;   // + one TMA producer warp
 constexpr uint32_t SLOT_BYTES = SLOT * 8;
-constexpr size_t SMEM_BYTES = (size_t)NSLOT * SLOT_BYTES + 128;
+constexpr size_t SMEM_BYTES = (size_t)NSLOT * SLOT_BYTES + 2 * NSLOT * 8;
 
 struct Params {
     double *u_next;
@@ -69,6 +70,9 @@ struct Params {
     uint64_t *sig_r;
     uint64_t sl, sr;
     unsigned int *counter;
+    // tuning knobs (DIOMP_STENCIL_PREVPF / DIOMP_STENCIL_CACHE)
+    int32_t prev_pf;      // u_prev tile L2 prefetch distance (output planes), 0 = off
+    int32_t cache;        // bit0: streaming (evict-first) u_next stores; bit1: evict-first u_prev loads
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -111,90 +115,136 @@ __device__ __forceinline__ double2 lds2(const double *p) {
     return *reinterpret_cast<const double2 *>(p);
 }
 
-__device__ __forceinline__ void store4(double *base, int64_t gi0, int64_t gi1, const double (&out)[4],
-                                       bool yv0, bool yv1, bool zv0, bool zv1) {
-    if (yv0 && zv1) *reinterpret_cast<double2 *>(base + gi0) = make_double2(out[0], out[1]);
-    else if (yv0 && zv0) base[gi0] = out[0];
-    if (yv1 && zv1) *reinterpret_cast<double2 *>(base + gi1) = make_double2(out[2], out[3]);
-    else if (yv1 && zv0) base[gi1] = out[2];
-}
-
 __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap *map, int z, int y, int x) {
     asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map),
                  "r"(z), "r"(y), "r"(x)
                  : "memory");
 }
 
-__device__ __forceinline__ double2 ldg2(const double *p) {
-    return __ldg(reinterpret_cast<const double2 *>(p));
-}
-
 __device__ __forceinline__ double tap(double acc, double w, double a, double b) {
     return __dadd_rn(acc, __dmul_rn(w, __dadd_rn(a, b)));
 }
 
-constexpr int PREV_PF = 6;  // u_prev planes prefetched into L2 ahead of use
+constexpr int PREV_PF = 4;  // u_prev tile prefetched into L2 this many output planes ahead
 
-// One loaded plane q for the thread's 2x2 points.  J is the register-window
-// rotation: window index t (0..8 = planes q-8..q) lives in bank (J+1+t)%9.
-// Per point the operation order is exactly the reference's; the 4 points are
-// interleaved tap by tap, which keeps only a sliding pair of neighbour rows
-// live (row -t / 1+t of tap t are rows 1-(t+1) / (t+1) of tap t+1).
-template <int J>
-__device__ __forceinline__ void step_plane(const Params &p, const double *__restrict__ sm,
-                                           uint64_t *bars, const CUtensorMap *map,
-                                           const CUtensorMap *pmap, double (&Q)[9][4], int q,
-                                           int L, int64_t xa, int y0, int z0, int ry, int zz,
-                                           bool yv0, bool yv1, bool zv0, bool zv1) {
-    const int s = q % NSLOT;
-    const int64_t o = q - 2 * R;  // output plane index within the chunk
-    const int64_t x = xa + o;
-    const int64_t y = y0 + ry, z = z0 + zz;
-    const int64_t gi0 = (x * p.NY + y) * p.NZ + z;
-    const int64_t gi1 = gi0 + p.NZ;
-    double pv[4] = {0.0, 0.0, 0.0, 0.0};
-    if (o >= 0) {  // u_prev of this output plane (L2-resident thanks to the TMA prefetch)
-        if (yv0 && zv1) { double2 v = ldg2(p.u_prev + gi0); pv[0] = v.x; pv[1] = v.y; }
-        else if (yv0 && zv0) pv[0] = __ldg(p.u_prev + gi0);
-        if (yv1 && zv1) { double2 v = ldg2(p.u_prev + gi1); pv[2] = v.x; pv[3] = v.y; }
-        else if (yv1 && zv0) pv[2] = __ldg(p.u_prev + gi1);
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Per-thread streaming state (pointers advance by one plane per output plane).
+struct Lane {
+    double *pn;         // u_next at (x, y, z) of the thread's first point
+    const double *pp;   // u_prev, same point
+    double *pl;         // left neighbour's ghost copy of pn (or null)
+    double *pr;         // right neighbour's ghost copy of pn (or null)
+    int64_t x;          // current output plane (full-array index)
+    int so;             // slot offset (doubles) of the thread's first point
+    int src_pt;         // which of the 4 points is the source (y/z match), -1: none
+    int cache;          // Params::cache
+    bool yv0, yv1, zv0, zv1, full;
+};
+
+__device__ __forceinline__ void st2_cs(double *p, double a, double b) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+__device__ __forceinline__ double2 ld2_ef(const double *p) {
+    double2 v;
+    asm volatile(
+        "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+        " ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n}\n"
+        : "=d"(v.x), "=d"(v.y)
+        : "l"(p));
+    return v;
+}
+
+template <bool FULL>
+__device__ __forceinline__ void store4(double *b, int64_t NZ, const double (&o)[4], const Lane &ln) {
+    if (FULL) {
+        if (ln.cache & 1) {
+            st2_cs(b, o[0], o[1]);
+            st2_cs(b + NZ, o[2], o[3]);
+        } else {
+            *reinterpret_cast<double2 *>(b) = make_double2(o[0], o[1]);
+            *reinterpret_cast<double2 *>(b + NZ) = make_double2(o[2], o[3]);
+        }
+        return;
     }
-    mbar_wait(&bars[s], (uint32_t)((q / NSLOT) & 1));
+    if (ln.yv0 && ln.zv1) *reinterpret_cast<double2 *>(b) = make_double2(o[0], o[1]);
+    else if (ln.yv0 && ln.zv0) b[0] = o[0];
+    if (ln.yv1 && ln.zv1) *reinterpret_cast<double2 *>(b + NZ) = make_double2(o[2], o[3]);
+    else if (ln.yv1 && ln.zv0) b[NZ] = o[2];
+}
+
+template <bool FULL>
+__device__ __forceinline__ void load4(const double *b, int64_t NZ, double (&v)[4], const Lane &ln) {
+    if (FULL) {
+        double2 a, c;
+        if (ln.cache & 2) {
+            a = ld2_ef(b);
+            c = ld2_ef(b + NZ);
+        } else {
+            a = __ldg(reinterpret_cast<const double2 *>(b));
+            c = __ldg(reinterpret_cast<const double2 *>(b + NZ));
+        }
+        v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
+        return;
+    }
+    v[0] = v[1] = v[2] = v[3] = 0.0;
+    if (ln.yv0 && ln.zv1) { double2 a = __ldg(reinterpret_cast<const double2 *>(b)); v[0] = a.x; v[1] = a.y; }
+    else if (ln.yv0 && ln.zv0) v[0] = __ldg(b);
+    if (ln.yv1 && ln.zv1) { double2 c = __ldg(reinterpret_cast<const double2 *>(b + NZ)); v[2] = c.x; v[3] = c.y; }
+    else if (ln.yv1 && ln.zv0) v[2] = __ldg(b + NZ);
+}
+
+// One loaded plane q for a compute thread's 2x2 points.  J is the
+// register-window rotation: window index t (0..8 = planes q-8..q) lives in
+// bank (J+1+t)%9.  Per point the operation order is exactly the reference's;
+// the 4 points are interleaved tap by tap, keeping only a sliding pair of
+// neighbour rows live (rows -t / 1+t of tap t are rows 1-(t+1) / (t+1) of
+// tap t+1).  The slot of plane q-R is released (empty barrier) after its
+// last use here.
+template <int J, bool FULL>
+__device__ __forceinline__ void step_plane(const Params &p, const double *sm, uint64_t *full,
+                                           uint64_t *empty, double (&Q)[9][4], double (&pv)[4],
+                                           Lane &ln, int q, int L) {
+    const int s = q % NSLOT;
+    const bool out_plane = q >= 2 * R;
+    double pn[4];
+    const bool more = q + 1 - 2 * R >= 0 && q + 1 < L;
+    if (more) load4<FULL>(ln.pp + (q + 1 - 2 * R) * p.NY * p.NZ, p.NZ, pn, ln);
+    mbar_wait(&full[s], (uint32_t)((q / NSLOT) & 1));
     {
-        const double *slot = sm + (size_t)s * SLOT + (R + ry) * BZ + R + zz;
-        double2 a = lds2(slot);
-        double2 b = lds2(slot + BZ);
+        const double *c = sm + s * SLOT + ln.so;
+        const double2 a = lds2(c), b = lds2(c + BZ);
         Q[J][0] = a.x; Q[J][1] = a.y; Q[J][2] = b.x; Q[J][3] = b.y;
     }
-    if (o >= 0) {
+    if (out_plane) {
         constexpr int C = (J + 5) % 9;  // centre bank
-        const double *cr = sm + (size_t)((q - R) % NSLOT) * SLOT + (R + ry) * BZ + R + zz;
+        const double *cr = sm + ((q - R) % NSLOT) * SLOT + ln.so;
         double acc[4];
 #pragma unroll
         for (int pt = 0; pt < 4; ++pt) acc[pt] = __dmul_rn(p.c0, Q[C][pt]);
-        // x taps from the register window
 #pragma unroll
         for (int t = 1; t <= R; ++t)
 #pragma unroll
             for (int pt = 0; pt < 4; ++pt)
                 acc[pt] = tap(acc[pt], p.wx[t], Q[(J + 5 + t) % 9][pt], Q[(J + 5 - t + 9) % 9][pt]);
-        // y taps: row a=0 needs rows +t,-t; row a=1 needs rows 1+t, 1-t
         {
             double2 rp0 = make_double2(Q[C][2], Q[C][3]);  // row +1 (own row 1)
             double2 rm1 = make_double2(Q[C][0], Q[C][1]);  // row 0  (own row 0)
 #pragma unroll
             for (int t = 1; t <= R; ++t) {
-                const double2 rm0 = lds2(cr - t * BZ);        // row -t
-                const double2 rp1 = lds2(cr + (1 + t) * BZ);  // row 1+t
+                const double2 rm0 = lds2(cr - t * BZ);
+                const double2 rp1 = lds2(cr + (1 + t) * BZ);
                 acc[0] = tap(acc[0], p.wy[t], rp0.x, rm0.x);
                 acc[1] = tap(acc[1], p.wy[t], rp0.y, rm0.y);
                 acc[2] = tap(acc[2], p.wy[t], rp1.x, rm1.x);
                 acc[3] = tap(acc[3], p.wy[t], rp1.y, rm1.y);
-                rp0 = rp1;  // row t+1 for a=0 at tap t+1
-                rm1 = rm0;  // row -t = 1-(t+1) for a=1 at tap t+1
+                rp0 = rp1;
+                rm1 = rm0;
             }
         }
-        // z taps per row: pairs (-4,-3) (-2,-1) [own 0,1] (2,3) (4,5)
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
             const double *rr = cr + a * BZ;
@@ -208,43 +258,57 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *__rest
         }
         double out[4];
 #pragma unroll
-        for (int pt = 0; pt < 4; ++pt) {
-            const double u = Q[C][pt];
-            double r = __dadd_rn(__dsub_rn(__dmul_rn(2.0, u), pv[pt]), acc[pt]);
-            if (p.src_x == x && p.src_y == y + (pt >> 1) && p.src_z == z + (pt & 1))
-                r = __dadd_rn(r, p.amp);
-            out[pt] = r;
+        for (int pt = 0; pt < 4; ++pt)
+            out[pt] = __dadd_rn(__dsub_rn(__dmul_rn(2.0, Q[C][pt]), pv[pt]), acc[pt]);
+        if (ln.src_pt >= 0 && ln.x == p.src_x) {
+#pragma unroll
+            for (int pt = 0; pt < 4; ++pt)
+                if (pt == ln.src_pt) out[pt] = __dadd_rn(out[pt], p.amp);
         }
-        // stores: local u_next, plus halo planes into the neighbours' ghosts
-        store4(p.u_next, gi0, gi1, out, yv0, yv1, zv0, zv1);
-        if (p.left_next && x < 2 * R)
-            store4(p.left_next + p.nxl * p.NY * p.NZ, gi0, gi1, out, yv0, yv1, zv0, zv1);
-        if (p.right_next && x >= p.nxl)
-            store4(p.right_next - p.nxl * p.NY * p.NZ, gi0, gi1, out, yv0, yv1, zv0, zv1);
+        store4<FULL>(ln.pn, p.NZ, out, ln);
+        if (ln.pl && ln.x < 2 * R) store4<FULL>(ln.pl, p.NZ, out, ln);
+        if (ln.pr && ln.x >= p.nxl) store4<FULL>(ln.pr, p.NZ, out, ln);
+        const int64_t ps = p.NY * p.NZ;
+        ln.pn += ps;
+        if (ln.pl) ln.pl += ps;
+        if (ln.pr) ln.pr += ps;
+        ln.x += 1;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        // slot of plane q-R is free now: refill it with plane q-R+NSLOT
-        if (q >= R && q - R + NSLOT < L) {
-            const int nq = q - R + NSLOT;
-            const int ns = nq % NSLOT;
-            mbar_expect_tx(&bars[ns], SLOT_BYTES);
-            tma_load_plane((double *)sm + (size_t)ns * SLOT, map, z0 - R, y0 - R,
-                           (int)(xa - R + nq), &bars[ns]);
-        }
-        // warm L2 with the u_prev tile PREV_PF output planes ahead
-        const int64_t po = o + 1 + PREV_PF;
-        if (po >= 0 && po < L - 2 * R) tma_prefetch_l2(pmap, z0, y0, (int)(xa + po));
+    if (more) {
+#pragma unroll
+        for (int pt = 0; pt < 4; ++pt) pv[pt] = pn[pt];
+    }
+    if (q >= R) {  // plane q-R had its last read (centre of this output plane)
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[(q - R) % NSLOT]);
     }
 }
 
-__global__ void __launch_bounds__(THREADS, 2)
+template <bool FULL>
+__device__ __forceinline__ void consume(const Params &p, const double *sm, uint64_t *full,
+                                       uint64_t *empty, Lane &ln, int L) {
+    double Q[9][4];
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) Q[i][j] = 0.0;
+    double pv[4];
+    load4<FULL>(ln.pp, p.NZ, pv, ln);  // u_prev of the first output plane
+#define DIOMP_STEP(JJ) \
+    if (q + JJ < L) step_plane<JJ, FULL>(p, sm, full, empty, Q, pv, ln, q + JJ, L);
+    for (int q = 0; q < L; q += 9) {
+        DIOMP_STEP(0) DIOMP_STEP(1) DIOMP_STEP(2) DIOMP_STEP(3) DIOMP_STEP(4)
+        DIOMP_STEP(5) DIOMP_STEP(6) DIOMP_STEP(7) DIOMP_STEP(8)
+    }
+#undef DIOMP_STEP
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
     stencil_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap pmap,
                        const __grid_constant__ Params p) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *sm = reinterpret_cast<double *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
-    __shared__ __align__(8) uint64_t bars[NSLOT];
+    extern __shared__ __align__(1024) double sm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + NSLOT * SLOT);
+    uint64_t *empty = full + NSLOT;
 
     // Unit decode: interior chunks first, the two edge chunks (which wait on
     // and write to the neighbours) last.
@@ -257,11 +321,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     int64_t xb = xa + p.chunk;
     if (xb > p.NX - R) xb = p.NX - R;
     const int L = (int)(xb - xa) + 2 * R;
-
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ry = 2 * warp, zz = 2 * lane;
-    const bool yv0 = y0 + ry < p.NY - R, yv1 = y0 + ry + 1 < p.NY - R;
-    const bool zv0 = z0 + zz < p.NZ - R, zv1 = z0 + zz + 1 < p.NZ - R;
 
     if (threadIdx.x == 0) {
         if (p.sync) {
@@ -270,34 +330,56 @@ __global__ void __launch_bounds__(THREADS, 2)
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
 #pragma unroll
-        for (int s = 0; s < NSLOT; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < NSLOT; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < NSLOT && q < L; ++q) {
-            mbar_expect_tx(&bars[q], SLOT_BYTES);
-            tma_load_plane(sm + (size_t)q * SLOT, &map, z0 - R, y0 - R, (int)(xa - R + q), &bars[q]);
+
+    if (warp == NCW) {
+        // ---- producer warp: TMA plane loads into the ring + u_prev L2 prefetch
+        if (lane == 0) {
+            const int nout = L - 2 * R;
+            const int pf = p.prev_pf;
+            for (int po = 0; po < pf && po < nout; ++po)
+                tma_prefetch_l2(&pmap, z0, y0, (int)(xa + po));
+            for (int q = 0; q < L; ++q) {
+                const int s = q % NSLOT;
+                if (q >= NSLOT) mbar_wait(&empty[s], (uint32_t)(((q / NSLOT) - 1) & 1));
+                mbar_expect_tx(&full[s], SLOT_BYTES);
+                tma_load_plane(sm + s * SLOT, &map, z0 - R, y0 - R, (int)(xa - R + q), &full[s]);
+                const int po = q - 2 * R + pf;
+                if (pf > 0 && po >= pf && po < nout) tma_prefetch_l2(&pmap, z0, y0, (int)(xa + po));
+            }
         }
-        for (int po = 0; po <= PREV_PF && po < L - 2 * R; ++po)
-            tma_prefetch_l2(&pmap, z0, y0, (int)(xa + po));
+    } else {
+        // ---- compute warps: 2 rows x 64 columns each, 2x2 points per thread
+        const int ry = 2 * warp, zz = 2 * lane;
+        const int64_t y = y0 + ry, z = z0 + zz;
+        Lane ln;
+        ln.yv0 = y < p.NY - R;
+        ln.yv1 = y + 1 < p.NY - R;
+        ln.zv0 = z < p.NZ - R;
+        ln.zv1 = z + 1 < p.NZ - R;
+        ln.full = (y0 + TY <= p.NY - R) && (z0 + TZ <= p.NZ - R);  // uniform per CTA
+        ln.so = (R + ry) * BZ + R + zz;
+        ln.cache = p.cache;
+        const int64_t g0 = (xa * p.NY + y) * p.NZ + z;
+        ln.pn = p.u_next + g0;
+        ln.pp = p.u_prev + g0;
+        ln.pl = p.left_next ? p.left_next + p.nxl * p.NY * p.NZ + g0 : nullptr;
+        ln.pr = p.right_next ? p.right_next - p.nxl * p.NY * p.NZ + g0 : nullptr;
+        ln.x = xa;
+        ln.src_pt = -1;
+        if (p.src_x >= xa && p.src_x < xb) {
+            const int64_t dy = p.src_y - y, dz = p.src_z - z;
+            if (dy >= 0 && dy < 2 && dz >= 0 && dz < 2) ln.src_pt = (int)(dy * 2 + dz);
+        }
+        if (ln.full) consume<true>(p, sm, full, empty, ln, L);
+        else consume<false>(p, sm, full, empty, ln, L);
     }
-
-    double Q[9][4];
-#pragma unroll
-    for (int i = 0; i < 9; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) Q[i][j] = 0.0;
-
-#define DIOMP_STEP(JJ)                                                                          \
-    if (q + JJ < L)                                                                             \
-        step_plane<JJ>(p, sm, bars, &map, &pmap, Q, q + JJ, L, xa, y0, z0, ry, zz, yv0, yv1, zv0, \
-                       zv1);
-    for (int q = 0; q < L; q += 9) {
-        DIOMP_STEP(0) DIOMP_STEP(1) DIOMP_STEP(2) DIOMP_STEP(3) DIOMP_STEP(4)
-        DIOMP_STEP(5) DIOMP_STEP(6) DIOMP_STEP(7) DIOMP_STEP(8)
-    }
-#undef DIOMP_STEP
 
     if (p.sync && last_cta_done(p.counter, gridDim.x) && threadIdx.x == 0) {
         if (p.sig_l) st_release_sys(p.sig_l, p.sl);
@@ -387,7 +469,7 @@ static bool fast_path_ok(uint64_t u_next, uint64_t u_cur, uint64_t u_prev, int64
 // Chunking along x: pick the chunk count minimising
 // rounds(units over resident CTA slots) x (chunk + warm-up cost).
 static void pick_chunks(int64_t nx_int, int ncols, int *chunk_out, int *nch_out) {
-    const int slots = kNumSMs * 2;
+    const int slots = kNumSMs;  // one CTA per SM
     const char *env = getenv("DIOMP_STENCIL_CHUNK");
     if (env && atoi(env) > 0) {
         int ch = atoi(env);
@@ -429,6 +511,10 @@ static int launch_fast(const CUtensorMap &map, const CUtensorMap &pmap, Params &
     p.ntz = (int)ceil_div(nz_int, TZ);
     p.ncols = nty * p.ntz;
     pick_chunks(nx_int, p.ncols, &p.chunk, &p.nch);
+    const char *pf = getenv("DIOMP_STENCIL_PREVPF");
+    p.prev_pf = pf ? atoi(pf) : PREV_PF;
+    const char *cm = getenv("DIOMP_STENCIL_CACHE");
+    p.cache = cm ? atoi(cm) : 0;
     const int64_t units = (int64_t)p.ncols * p.nch;
     if (units > 0x7fffffff) return DIOMP_BAD_REQUEST;
     stencil_tma_kernel<<<(unsigned)units, THREADS, SMEM_BYTES, s>>>(map, pmap, p);
