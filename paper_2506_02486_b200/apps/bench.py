@@ -185,19 +185,31 @@ def run_collective(rt: Runtime, spec: BenchSpec, comm=None) -> list[BenchRow]:
     vals = np.random.default_rng(1000 + rt.rank).uniform(-1, 1, max_size // 4).astype(np.float32)
     rt.gm.view(0, send.addr.offset, vals.nbytes)[:] = vals.tobytes()
     rows: list[BenchRow] = []
+    timer = _Timer(rt)
+    device_timed = comm.device_sync
+
+    def run_once(size, blocking):
+        if spec.kind is BenchKind.Bcast:
+            coll.bcast(comm, send.addr, size, root=0, blocking=blocking)
+        else:
+            coll.allreduce(comm, send.addr, recv.addr, size // 4, op, blocking=blocking)
+
     for size in spec.sizes:
-        def run_once():
-            if spec.kind is BenchKind.Bcast:
-                coll.bcast(comm, send.addr, size, root=0)
-            else:
-                coll.allreduce(comm, send.addr, recv.addr, size // 4, op)
         for _ in range(spec.warmup):
-            run_once()
+            run_once(size, True)
         rt.barrier(rt.world)
-        t0 = time.perf_counter()
-        for _ in range(spec.iters):
-            run_once()
-        elapsed = time.perf_counter() - t0
+        if device_timed:
+            # enqueue-only repetitions, CUDA events on the RMA stream (device time)
+            timer.start()
+            for _ in range(spec.iters):
+                run_once(size, False)
+            elapsed = timer.stop_ms() / 1e3
+            _native.check_device(rt.gpus[0], "collective bench")
+        else:
+            t0 = time.perf_counter()
+            for _ in range(spec.iters):
+                run_once(size, True)
+            elapsed = time.perf_counter() - t0
         got = rt.ctrl.allgather(tuple(range(rt.nranks)), "collbench", pickle.dumps(elapsed))
         elapsed = max(pickle.loads(b) for _, b in got)
         if rt.rank == 0:

@@ -135,17 +135,23 @@ def bootstrap(rt: Runtime, group: Group) -> Communicator:
 # ---------------------------------------------------------------------------
 
 def _team(comm: Communicator, pos: int, sync: int) -> _native.Team:
+    """Team descriptor of ring position `pos` (cached; epochs refreshed)."""
     rt = comm.rt
-    t = _native.Team()
-    t.k, t.pos, t.sync = comm.size, pos, sync
+    cache = comm.__dict__.setdefault("_teams", {})
+    t = cache.get((pos, sync))
     me_ep = comm.ring[pos]
-    t.device = rt.gpus[me_ep.device]
-    t.flag_off = rt.flag_offset
-    t.counter_off = rt.scratch_offset + COUNTER_OFF + 64 * COUNTER_COLL
     me = rt.endpoint_index(me_ep.rank, me_ep.device)
-    for q, ep in enumerate(comm.ring):
-        t.base[q] = rt.peer_address(ep.rank, ep.device)
-        t.slot[q] = rt.endpoint_index(ep.rank, ep.device)
+    if t is None:
+        t = _native.Team()
+        t.k, t.pos, t.sync = comm.size, pos, sync
+        t.device = rt.gpus[me_ep.device]
+        t.flag_off = rt.flag_offset
+        t.counter_off = rt.scratch_offset + COUNTER_OFF + 64 * COUNTER_COLL
+        for q, ep in enumerate(comm.ring):
+            t.base[q] = rt.peer_address(ep.rank, ep.device)
+            t.slot[q] = rt.endpoint_index(ep.rank, ep.device)
+        cache[(pos, sync)] = t
+    for q in range(comm.size):
         if q != pos:
             t.epoch_to[q], t.epoch_from[q] = rt.pair_epochs(me, t.slot[q])
     return t
@@ -159,12 +165,17 @@ def _after_torch(rt: Runtime, device: int):
     torch.cuda.current_stream(gpu).synchronize()
 
 
-def _run(comm: Communicator, launch):
-    """launch(team, stream) for every local position, device- or host-synchronised."""
+def _run(comm: Communicator, launch, blocking: bool = True):
+    """launch(team, stream) for every local position, device- or host-synchronised.
+    blocking=False (device-synchronised rings only) enqueues and returns: the
+    result is ready once the rank's RMA stream of that device has drained."""
     rt = comm.rt
     sync = 1 if (comm.device_sync and comm.size > 1) else 0
-    for pos in comm.my_positions:
-        _after_torch(rt, comm.ring[pos].device)
+    if not sync:
+        blocking = True
+    if blocking:
+        for pos in comm.my_positions:
+            _after_torch(rt, comm.ring[pos].device)
     if not sync and comm.size > 1:
         rt.barrier(comm.group)
     used = []
@@ -173,9 +184,10 @@ def _run(comm: Communicator, launch):
         s = rt._rma_streams[ep.device]
         _native.check(launch(_team(comm, pos, sync), s.handle), "collective launch")
         used.append((pos, s))
-    for pos, s in used:
-        s.synchronize()
-        _native.check_device(s.gpu, "collective")
+    if blocking:
+        for pos, s in used:
+            s.synchronize()
+            _native.check_device(s.gpu, "collective")
     if sync:
         for pos in comm.my_positions:
             me_ep = comm.ring[pos]
@@ -200,7 +212,8 @@ def _check_typed(buffer: GlobalAddress, count: int, etype: ElementType):
 # collectives
 # ---------------------------------------------------------------------------
 
-def bcast(comm: Communicator, buffer: GlobalAddress, nbytes: int, root: int = 0):
+def bcast(comm: Communicator, buffer: GlobalAddress, nbytes: int, root: int = 0, *,
+          blocking: bool = True):
     """Every member's buffer ends equal to the root member's buffer at entry."""
     rt, k = comm.rt, comm.size
     if not 0 <= root < k:
@@ -211,11 +224,11 @@ def bcast(comm: Communicator, buffer: GlobalAddress, nbytes: int, root: int = 0)
     if k == 1 or nbytes == 0:
         return
     comm._next_seq()
-    _run(comm, lambda t, s: _native.lib.diomp_bcast(t, buffer.offset, nbytes, root, s))
+    _run(comm, lambda t, s: _native.lib.diomp_bcast(t, buffer.offset, nbytes, root, s), blocking)
 
 
 def reduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, count: int,
-           op: ReduceOp, root: int = 0):
+           op: ReduceOp, root: int = 0, *, blocking: bool = True):
     """Ring-ordered reduction to the root member; non-root recv untouched."""
     rt, k = comm.rt, comm.size
     if not 0 <= root < k:
@@ -242,11 +255,11 @@ def reduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, count: 
         return
     comm._next_seq()
     _run(comm, lambda t, s: _native.lib.diomp_reduce(t, send.offset, recv.offset, count,
-                                                     op.etype.code, op.code, root, s))
+                                                     op.etype.code, op.code, root, s), blocking)
 
 
 def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, count: int,
-              op: ReduceOp):
+              op: ReduceOp, *, blocking: bool = True):
     """Reduce-scatter in ring-fold order + all-gather; in place works."""
     rt, k = comm.rt, comm.size
     _check_typed(send, count, op.etype)
@@ -270,7 +283,7 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
         return
     comm._next_seq()
     _run(comm, lambda t, s: _native.lib.diomp_allreduce(t, send.offset, recv.offset, count,
-                                                        op.etype.code, op.code, s))
+                                                        op.etype.code, op.code, s), blocking)
 
 
 def device_bcast(rt: Runtime, var: GlobalAddress, nbytes: int, group: Group):

@@ -41,11 +41,16 @@ constexpr int TZ = 64;
 constexpr int BY = TY + 2 * R;  // 24 rows per slot
 constexpr int BZ = TZ + 2 * R;  // 72 columns per slot
 constexpr int SLOT = BY * BZ;   // doubles per slot
-constexpr int NSLOT = 16;                 // plane ring: 5 in use + 11 in flight
+constexpr int NSLOT = 11;                 // u_cur plane ring: 5 in use + 6 in flight
+constexpr int NPREV = 8;                  // u_prev tile ring
+constexpr int PREV_AHEAD = NPREV - 2;     // u_prev tiles issued this many outputs ahead
+constexpr int PSLOT = TY * TZ;            // doubles per u_prev tile
 constexpr int NCW = 8;                    // compute warps (2 rows each)
 constexpr int THREADS = (NCW + 1) * 32;   // + one TMA producer warp
 constexpr uint32_t SLOT_BYTES = SLOT * 8;
-constexpr size_t SMEM_BYTES = (size_t)NSLOT * SLOT_BYTES + 2 * NSLOT * 8;
+constexpr uint32_t PSLOT_BYTES = PSLOT * 8;
+constexpr size_t SMEM_BYTES =
+    (size_t)NSLOT * SLOT_BYTES + (size_t)NPREV * PSLOT_BYTES + 2 * (NSLOT + NPREV) * 8;
 
 struct Params {
     double *u_next;
@@ -109,6 +114,28 @@ __device__ __forceinline__ void tma_load_plane(double *dst, const CUtensorMap *m
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"(map), "r"(z), "r"(y), "r"(x), "r"(smem_u32(bar))
         : "memory");
+}
+
+// Same with an L2 eviction-priority policy (createpolicy result).
+__device__ __forceinline__ void tma_load_plane_hint(double *dst, const CUtensorMap *map, int z,
+                                                    int y, int x, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(z), "r"(y), "r"(x), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 
 __device__ __forceinline__ double2 lds2(const double *p) {
@@ -206,13 +233,11 @@ __device__ __forceinline__ void load4(const double *b, int64_t NZ, double (&v)[4
 // last use here.
 template <int J, bool FULL>
 __device__ __forceinline__ void step_plane(const Params &p, const double *sm, uint64_t *full,
-                                           uint64_t *empty, double (&Q)[9][4], double (&pv)[4],
-                                           Lane &ln, int q, int L) {
+                                           uint64_t *empty, const double *psm, uint64_t *pfull,
+                                           uint64_t *pempty, double (&Q)[9][4], Lane &ln, int q,
+                                           int L) {
     const int s = q % NSLOT;
     const bool out_plane = q >= 2 * R;
-    double pn[4];
-    const bool more = q + 1 - 2 * R >= 0 && q + 1 < L;
-    if (more) load4<FULL>(ln.pp + (q + 1 - 2 * R) * p.NY * p.NZ, p.NZ, pn, ln);
     mbar_wait(&full[s], (uint32_t)((q / NSLOT) & 1));
     {
         const double *c = sm + s * SLOT + ln.so;
@@ -256,6 +281,15 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
             c0 = tap(c0, p.wz[3], p23.y, m43.y); c1 = tap(c1, p.wz[3], p45.x, m21.x);
             c0 = tap(c0, p.wz[4], p45.x, m43.x); c1 = tap(c1, p.wz[4], p45.y, m43.y);
         }
+        // u_prev of this output plane from its TMA-filled tile, then free the tile
+        const int o = q - 2 * R;
+        const int ps = o % NPREV;
+        mbar_wait(&pfull[ps], (uint32_t)((o / NPREV) & 1));
+        const double *pt0 = psm + ps * PSLOT + (ln.so / BZ - R) * TZ + (ln.so % BZ - R);
+        const double2 pa = lds2(pt0), pb = lds2(pt0 + TZ);
+        const double pv[4] = {pa.x, pa.y, pb.x, pb.y};
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&pempty[ps]);
         double out[4];
 #pragma unroll
         for (int pt = 0; pt < 4; ++pt)
@@ -268,15 +302,11 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
         store4<FULL>(ln.pn, p.NZ, out, ln);
         if (ln.pl && ln.x < 2 * R) store4<FULL>(ln.pl, p.NZ, out, ln);
         if (ln.pr && ln.x >= p.nxl) store4<FULL>(ln.pr, p.NZ, out, ln);
-        const int64_t ps = p.NY * p.NZ;
-        ln.pn += ps;
-        if (ln.pl) ln.pl += ps;
-        if (ln.pr) ln.pr += ps;
+        const int64_t pstride = p.NY * p.NZ;
+        ln.pn += pstride;
+        if (ln.pl) ln.pl += pstride;
+        if (ln.pr) ln.pr += pstride;
         ln.x += 1;
-    }
-    if (more) {
-#pragma unroll
-        for (int pt = 0; pt < 4; ++pt) pv[pt] = pn[pt];
     }
     if (q >= R) {  // plane q-R had its last read (centre of this output plane)
         __syncwarp();
@@ -286,16 +316,16 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
 
 template <bool FULL>
 __device__ __forceinline__ void consume(const Params &p, const double *sm, uint64_t *full,
-                                       uint64_t *empty, Lane &ln, int L) {
+                                       uint64_t *empty, const double *psm, uint64_t *pfull,
+                                       uint64_t *pempty, Lane &ln, int L) {
     double Q[9][4];
 #pragma unroll
     for (int i = 0; i < 9; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) Q[i][j] = 0.0;
-    double pv[4];
-    load4<FULL>(ln.pp, p.NZ, pv, ln);  // u_prev of the first output plane
 #define DIOMP_STEP(JJ) \
-    if (q + JJ < L) step_plane<JJ, FULL>(p, sm, full, empty, Q, pv, ln, q + JJ, L);
+    if (q + JJ < L) \
+        step_plane<JJ, FULL>(p, sm, full, empty, psm, pfull, pempty, Q, ln, q + JJ, L);
     for (int q = 0; q < L; q += 9) {
         DIOMP_STEP(0) DIOMP_STEP(1) DIOMP_STEP(2) DIOMP_STEP(3) DIOMP_STEP(4)
         DIOMP_STEP(5) DIOMP_STEP(6) DIOMP_STEP(7) DIOMP_STEP(8)
@@ -307,8 +337,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     stencil_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap pmap,
                        const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) double sm[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(sm + NSLOT * SLOT);
+    double *psm = sm + NSLOT * SLOT;                      // u_prev tiles
+    uint64_t *full = reinterpret_cast<uint64_t *>(psm + NPREV * PSLOT);
     uint64_t *empty = full + NSLOT;
+    uint64_t *pfull = empty + NSLOT;
+    uint64_t *pempty = pfull + NPREV;
 
     // Unit decode: interior chunks first, the two edge chunks (which wait on
     // and write to the neighbours) last.
@@ -334,6 +367,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NCW);
         }
+#pragma unroll
+        for (int s = 0; s < NPREV; ++s) {
+            mbar_init(&pfull[s], 1);
+            mbar_init(&pempty[s], NCW);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -342,16 +380,31 @@ __global__ void __launch_bounds__(THREADS, 1)
         // ---- producer warp: TMA plane loads into the ring + u_prev L2 prefetch
         if (lane == 0) {
             const int nout = L - 2 * R;
-            const int pf = p.prev_pf;
-            for (int po = 0; po < pf && po < nout; ++po)
-                tma_prefetch_l2(&pmap, z0, y0, (int)(xa + po));
+            const uint64_t pol_cur = policy_evict_last(), pol_prev = policy_evict_first();
+            const bool hint_cur = p.cache & 4, hint_prev = p.cache & 8;
+            auto issue_prev = [&](int o) {  // u_prev tile of output plane o
+                const int ps = o % NPREV;
+                if (o >= NPREV) mbar_wait(&pempty[ps], (uint32_t)(((o / NPREV) - 1) & 1));
+                mbar_expect_tx(&pfull[ps], PSLOT_BYTES);
+                if (hint_prev)
+                    tma_load_plane_hint(psm + ps * PSLOT, &pmap, z0, y0, (int)(xa + o), &pfull[ps],
+                                        pol_prev);
+                else
+                    tma_load_plane(psm + ps * PSLOT, &pmap, z0, y0, (int)(xa + o), &pfull[ps]);
+            };
+            int next_prev = 0;
             for (int q = 0; q < L; ++q) {
                 const int s = q % NSLOT;
                 if (q >= NSLOT) mbar_wait(&empty[s], (uint32_t)(((q / NSLOT) - 1) & 1));
                 mbar_expect_tx(&full[s], SLOT_BYTES);
-                tma_load_plane(sm + s * SLOT, &map, z0 - R, y0 - R, (int)(xa - R + q), &full[s]);
-                const int po = q - 2 * R + pf;
-                if (pf > 0 && po >= pf && po < nout) tma_prefetch_l2(&pmap, z0, y0, (int)(xa + po));
+                if (hint_cur)
+                    tma_load_plane_hint(sm + s * SLOT, &map, z0 - R, y0 - R, (int)(xa - R + q),
+                                        &full[s], pol_cur);
+                else
+                    tma_load_plane(sm + s * SLOT, &map, z0 - R, y0 - R, (int)(xa - R + q), &full[s]);
+                // keep u_prev PREV_AHEAD output planes ahead of the plane that completes
+                for (; next_prev < nout && next_prev <= q - 2 * R + PREV_AHEAD; ++next_prev)
+                    issue_prev(next_prev);
             }
         }
     } else {
@@ -377,8 +430,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int64_t dy = p.src_y - y, dz = p.src_z - z;
             if (dy >= 0 && dy < 2 && dz >= 0 && dz < 2) ln.src_pt = (int)(dy * 2 + dz);
         }
-        if (ln.full) consume<true>(p, sm, full, empty, ln, L);
-        else consume<false>(p, sm, full, empty, ln, L);
+        if (ln.full) consume<true>(p, sm, full, empty, psm, pfull, pempty, ln, L);
+        else consume<false>(p, sm, full, empty, psm, pfull, pempty, ln, L);
     }
 
     if (p.sync && last_cta_done(p.counter, gridDim.x) && threadIdx.x == 0) {
@@ -451,9 +504,17 @@ static int make_plane_map(CUtensorMap *map, const double *u, int64_t NX, int64_t
     cuuint64_t strides[2] = {(cuuint64_t)NZ * 8, (cuuint64_t)NY * NZ * 8};
     cuuint32_t box[3] = {halo ? (cuuint32_t)BZ : (cuuint32_t)TZ, halo ? (cuuint32_t)BY : (cuuint32_t)TY, 1};
     cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (const char *e = getenv("DIOMP_STENCIL_PROMO")) {
+        const int v = atoi(e);
+        promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                         : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
     CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)u, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? DIOMP_OK : DIOMP_BAD_REQUEST;
 }
 
