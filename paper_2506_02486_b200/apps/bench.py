@@ -135,6 +135,8 @@ def run_p2p(rt: Runtime, spec: BenchSpec) -> list[BenchRow]:
             rows.append(BenchRow(spec.kind.value + ("_d2d" if d2d else ""), size, reps,
                                  elapsed / reps * 1e6, size * reps / elapsed / MIB, wire))
     rt.barrier(rt.world)
+    rt.free(src)
+    rt.free(buf)
     return rows
 
 

@@ -133,9 +133,9 @@ class CannonRing:
             fwd, sync = 0, None
             if p > 1:
                 pred = self.world[(e - 1) % p]
+                # always forward (also on the last step, as cannon.py:124-131 does):
+                # after P steps every stripe is back home, so runs can repeat
                 fwd = rt.peer_address(pred.rank, pred.device, self.bufs[d][(t + 1) % 2].addr.offset)
-                if t == p - 1:
-                    fwd = 0  # the last step's stripe is not needed again
             if self.sync:
                 me = rt.endpoint_index(ep.rank, ep.device)
                 nbrs = []
