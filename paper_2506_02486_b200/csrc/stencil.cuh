@@ -235,10 +235,12 @@ template <int J, bool FULL>
 __device__ __forceinline__ void step_plane(const Params &p, const double *sm, uint64_t *full,
                                            uint64_t *empty, const double *psm, uint64_t *pfull,
                                            uint64_t *pempty, double (&Q)[9][4], Lane &ln, int q,
-                                           int L) {
-    const int s = q % NSLOT;
+                                           int L, int &s, uint32_t &ph) {
+    // s / ph: ring slot and mbarrier phase of plane q (advanced incrementally,
+    // no division by NSLOT); the centre plane q-R sits R slots behind.
     const bool out_plane = q >= 2 * R;
-    mbar_wait(&full[s], (uint32_t)((q / NSLOT) & 1));
+    const int sc = s >= R ? s - R : s - R + NSLOT;
+    mbar_wait(&full[s], ph);
     {
         const double *c = sm + s * SLOT + ln.so;
         const double2 a = lds2(c), b = lds2(c + BZ);
@@ -246,7 +248,7 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
     }
     if (out_plane) {
         constexpr int C = (J + 5) % 9;  // centre bank
-        const double *cr = sm + ((q - R) % NSLOT) * SLOT + ln.so;
+        const double *cr = sm + sc * SLOT + ln.so;
         double acc[4];
 #pragma unroll
         for (int pt = 0; pt < 4; ++pt) acc[pt] = __dmul_rn(p.c0, Q[C][pt]);
@@ -310,7 +312,11 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
     }
     if (q >= R) {  // plane q-R had its last read (centre of this output plane)
         __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[(q - R) % NSLOT]);
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[sc]);
+    }
+    if (++s == NSLOT) {
+        s = 0;
+        ph ^= 1u;
     }
 }
 
@@ -323,9 +329,11 @@ __device__ __forceinline__ void consume(const Params &p, const double *sm, uint6
     for (int i = 0; i < 9; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) Q[i][j] = 0.0;
+    int s = 0;
+    uint32_t ph = 0;
 #define DIOMP_STEP(JJ) \
     if (q + JJ < L) \
-        step_plane<JJ, FULL>(p, sm, full, empty, psm, pfull, pempty, Q, ln, q + JJ, L);
+        step_plane<JJ, FULL>(p, sm, full, empty, psm, pfull, pempty, Q, ln, q + JJ, L, s, ph);
     for (int q = 0; q < L; q += 9) {
         DIOMP_STEP(0) DIOMP_STEP(1) DIOMP_STEP(2) DIOMP_STEP(3) DIOMP_STEP(4)
         DIOMP_STEP(5) DIOMP_STEP(6) DIOMP_STEP(7) DIOMP_STEP(8)
