@@ -9,8 +9,9 @@
 // 2. diomp_dgemm -- the Cannon block product of apps/cannon.py:138
 //    (C += A_blk @ B_s, BLAS in the reference, tolerance-checked).  tcgen05
 //    has no f64 kind, so the FP64 tensor path on Blackwell is DMMA
-//    (mma.sync.m8n8k4.f64).  128x128x16 CTA tiles, 8 warps of 64x32, 4-stage
-//    cp.async pipeline into bank-conflict-free padded tiles.  When `fwd` is
+//    (mma.sync.m8n8k4.f64; the larger f64 shapes expand to the same DMMA.8x8x4
+//    on sm_100a).  Default tiles 128x64x16, 8 warps of 32x32, 2 CTAs/SM,
+//    3-stage cp.async pipeline into bank-conflict-free padded tiles.  When `fwd` is
 //    set, every B tile is additionally stored once to the predecessor's spare
 //    stripe over NVLink straight from shared memory (CTA row mi forwards the
 //    k-tiles kt with kt % n_mtiles == mi), fusing the ring shift of
@@ -77,14 +78,22 @@ __global__ void __launch_bounds__(256) matmul_exact_kernel(int64_t n, int64_t kk
 // ---------------------------------------------------------------------------
 // DMMA DGEMM: C += A @ B
 // ---------------------------------------------------------------------------
-constexpr int BM = 128, BN = 128, BK = 16;
-constexpr int APAD = BK + 4;   // A tile row pitch (doubles): conflict-free fragment loads
-constexpr int BPAD = BN + 4;   // B tile row pitch
-constexpr int STAGES = 4;
-constexpr int GTHREADS = 256;
-constexpr int A_STAGE = BM * APAD;
-constexpr int B_STAGE = BK * BPAD;
-constexpr size_t GEMM_SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+// Tile configurations.  WM x WN = 8x8 DMMA fragments per warp; WARPS_M x
+// WARPS_N warps per CTA; MINB CTAs per SM (register budget).
+template <int WM_, int WN_, int WARPS_M_, int WARPS_N_, int BK_, int STAGES_, int MINB_>
+struct Cfg {
+    static constexpr int WM = WM_, WN = WN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+    static constexpr int BM = WM * 8 * WARPS_M, BN = WN * 8 * WARPS_N, BK = BK_;
+    static constexpr int STAGES = STAGES_, MINB = MINB_;
+    static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+    static constexpr int APAD = BK + 4;   // A tile row pitch (doubles): conflict-free fragments
+    static constexpr int BPAD = BN + 4;   // B tile row pitch
+    static constexpr int A_STAGE = BM * APAD, B_STAGE = BK * BPAD;
+    static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+};
+using CfgBig = Cfg<8, 4, 2, 4, 16, 4, 1>;    // 128x128 CTA, 64x32 warps, 1 CTA/SM
+using CfgDual = Cfg<4, 4, 4, 2, 16, 3, 2>;   // 128x64 CTA, 32x32 warps, 2 CTAs/SM
+using CfgDeepK = Cfg<8, 4, 2, 4, 32, 3, 1>;  // 128x128 CTA, BK=32 (half the barriers)
 
 struct GemmParams {
     int64_t M, N, K;
@@ -119,34 +128,40 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+template <class C>
 __device__ __forceinline__ void load_tiles(const GemmParams &p, double *As, double *Bs, int64_t m0,
                                            int64_t n0, int64_t k0) {
-    // A: BM x BK = 128 rows x 8 chunks of 16 B; B: BK x BN = 16 rows x 64 chunks
+    // A: BM x BK in 16 B chunks; B: BK x BN in 16 B chunks (trip counts are
+    // compile-time so the loops unroll)
+    constexpr int NA = C::BM * C::BK / 2, NB = C::BK * C::BN / 2;
 #pragma unroll
-    for (int it = 0; it < (BM * BK / 2) / GTHREADS; ++it) {
-        const int e = threadIdx.x + it * GTHREADS;
-        const int r = e / (BK / 2), ch = e % (BK / 2);
+    for (int it = 0; it < (NA + C::THREADS - 1) / C::THREADS; ++it) {
+        const int e = threadIdx.x + it * C::THREADS;
+        if (NA % C::THREADS && e >= NA) break;
+        const int r = e / (C::BK / 2), ch = e % (C::BK / 2);
         const int64_t gr = m0 + r, gk = k0 + ch * 2;
         const bool ok = gr < p.M && gk < p.K;
-        cp_async16(As + r * APAD + ch * 2, ok ? (const void *)(p.A + gr * p.lda + gk) : (const void *)p.A, ok);
+        cp_async16(As + r * C::APAD + ch * 2, ok ? (const void *)(p.A + gr * p.lda + gk) : (const void *)p.A, ok);
     }
 #pragma unroll
-    for (int it = 0; it < (BK * BN / 2) / GTHREADS; ++it) {
-        const int e = threadIdx.x + it * GTHREADS;
-        const int r = e / (BN / 2), ch = e % (BN / 2);
+    for (int it = 0; it < (NB + C::THREADS - 1) / C::THREADS; ++it) {
+        const int e = threadIdx.x + it * C::THREADS;
+        if (NB % C::THREADS && e >= NB) break;
+        const int r = e / (C::BN / 2), ch = e % (C::BN / 2);
         const int64_t gk = k0 + r, gn = n0 + ch * 2;
         const bool ok = gk < p.K && gn < p.N;
-        cp_async16(Bs + r * BPAD + ch * 2, ok ? (const void *)(p.B + gk * p.ldb + gn) : (const void *)p.B, ok);
+        cp_async16(Bs + r * C::BPAD + ch * 2, ok ? (const void *)(p.B + gk * p.ldb + gn) : (const void *)p.B, ok);
     }
 }
 
-__global__ void __launch_bounds__(GTHREADS, 1) dgemm_dmma_kernel(const __grid_constant__ GemmParams p) {
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_dmma_kernel(const __grid_constant__ GemmParams p) {
     extern __shared__ __align__(16) double gsm[];
     double *As = gsm;
-    double *Bs = gsm + STAGES * A_STAGE;
+    double *Bs = gsm + C::STAGES * C::A_STAGE;
 
     // swizzle CTAs in groups of 8 m-tiles for L2 reuse of B
-    const int64_t mtiles = ceil_div(p.M, BM), ntiles = ceil_div(p.N, BN);
+    const int64_t mtiles = ceil_div(p.M, C::BM), ntiles = ceil_div(p.N, C::BN);
     const int64_t bid = blockIdx.x;
     const int64_t group = 8;
     const int64_t per_group = group * ntiles;
@@ -155,7 +170,7 @@ __global__ void __launch_bounds__(GTHREADS, 1) dgemm_dmma_kernel(const __grid_co
     const int64_t gsize = (mtiles - first_m) < group ? (mtiles - first_m) : group;
     const int64_t mi = first_m + (bid % per_group) % gsize;
     const int64_t ni = (bid % per_group) / gsize;
-    const int64_t m0 = mi * BM, n0 = ni * BN;
+    const int64_t m0 = mi * C::BM, n0 = ni * C::BN;
 
     if (p.sync) {
         if (threadIdx.x < 2 && p.wait_addr[threadIdx.x])
@@ -164,64 +179,64 @@ __global__ void __launch_bounds__(GTHREADS, 1) dgemm_dmma_kernel(const __grid_co
     }
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+    const int wm = (warp / C::WARPS_N) * C::WM * 8, wn = (warp % C::WARPS_N) * C::WN * 8;
     const int gq = lane >> 2, tq = lane & 3;
 
-    double acc[8][4][2];
+    double acc[C::WM][C::WN][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < C::WM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < C::WN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    const int64_t ktiles = ceil_div(p.K, BK);
+    const int64_t ktiles = ceil_div(p.K, C::BK);
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < ktiles) load_tiles(p, As + s * A_STAGE, Bs + s * B_STAGE, m0, n0, (int64_t)s * BK);
+    for (int s = 0; s < C::STAGES - 1; ++s) {
+        if (s < ktiles) load_tiles<C>(p, As + s * C::A_STAGE, Bs + s * C::B_STAGE, m0, n0, (int64_t)s * C::BK);
         cp_async_commit();
     }
     for (int64_t kt = 0; kt < ktiles; ++kt) {
-        cp_async_wait<STAGES - 2>();
+        cp_async_wait<C::STAGES - 2>();
         __syncthreads();
-        const int st = (int)(kt % STAGES);
-        const double *a_s = As + st * A_STAGE;
-        const double *b_s = Bs + st * B_STAGE;
+        const int st = (int)(kt % C::STAGES);
+        const double *a_s = As + st * C::A_STAGE;
+        const double *b_s = Bs + st * C::B_STAGE;
         // prefetch tile kt + STAGES - 1 into the slot consumed at kt-1
-        const int64_t nk = kt + STAGES - 1;
+        const int64_t nk = kt + C::STAGES - 1;
         if (nk < ktiles) {
-            const int ns = (int)(nk % STAGES);
-            load_tiles(p, As + ns * A_STAGE, Bs + ns * B_STAGE, m0, n0, nk * BK);
+            const int ns = (int)(nk % C::STAGES);
+            load_tiles<C>(p, As + ns * C::A_STAGE, Bs + ns * C::B_STAGE, m0, n0, nk * C::BK);
         }
         cp_async_commit();
         // fused ring shift: forward this B tile once to the predecessor
         if (p.fwd && (kt % mtiles) == mi) {
-            for (int e = threadIdx.x; e < BK * BN / 2; e += GTHREADS) {
-                const int r = e / (BN / 2), ch = e % (BN / 2);
-                const int64_t gk = kt * BK + r, gn = n0 + ch * 2;
+            for (int e = threadIdx.x; e < C::BK * C::BN / 2; e += C::THREADS) {
+                const int r = e / (C::BN / 2), ch = e % (C::BN / 2);
+                const int64_t gk = kt * C::BK + r, gn = n0 + ch * 2;
                 if (gk < p.K && gn < p.N)
                     *reinterpret_cast<double2 *>(p.fwd + gk * p.ldf + gn) =
-                        *reinterpret_cast<const double2 *>(b_s + r * BPAD + ch * 2);
+                        *reinterpret_cast<const double2 *>(b_s + r * C::BPAD + ch * 2);
             }
         }
 #pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            double af[8], bf[4];
+        for (int kk = 0; kk < C::BK; kk += 4) {
+            double af[C::WM], bf[C::WN];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) af[i] = a_s[(wm + i * 8 + gq) * APAD + kk + tq];
+            for (int i = 0; i < C::WM; ++i) af[i] = a_s[(wm + i * 8 + gq) * C::APAD + kk + tq];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = b_s[(kk + tq) * BPAD + wn + j * 8 + gq];
+            for (int j = 0; j < C::WN; ++j) bf[j] = b_s[(kk + tq) * C::BPAD + wn + j * 8 + gq];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < C::WM; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+                for (int j = 0; j < C::WN; ++j) dmma(acc[i][j], af[i], bf[j]);
         }
     }
     cp_async_wait<0>();
 
     // epilogue: C = C + acc (numpy's `C += A_blk @ B` order: product, then add)
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < C::WM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < C::WN; ++j) {
             const int64_t r = m0 + wm + i * 8 + gq;
             const int64_t cidx = n0 + wn + j * 8 + tq * 2;
             if (r < p.M && cidx + 1 < p.N) {
@@ -237,6 +252,20 @@ __global__ void __launch_bounds__(GTHREADS, 1) dgemm_dmma_kernel(const __grid_co
 
     if (p.sync && last_cta_done(p.counter, gridDim.x) && threadIdx.x < 2 && p.sig_addr[threadIdx.x])
         st_release_sys(p.sig_addr[threadIdx.x], p.sig_value[threadIdx.x]);
+}
+
+template <class C>
+static int launch_dgemm(const GemmParams &p, int device, cudaStream_t s) {
+    static bool attr_set[64] = {false};
+    if (device < 64 && !attr_set[device]) {
+        DIOMP_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)C::SMEM));
+        attr_set[device] = true;
+    }
+    const int64_t tiles = ceil_div(p.M, C::BM) * ceil_div(p.N, C::BN);
+    dgemm_dmma_kernel<C><<<(unsigned)tiles, C::THREADS, C::SMEM, s>>>(p);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
 }
 
 }  // namespace gemm
@@ -266,12 +295,6 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
         ((x->A | x->B | x->C | x->fwd) & 15) || (x->fwd && (x->ldf & 1)))
         return DIOMP_BAD_REQUEST;
     DIOMP_CUDA_TRY(cudaSetDevice(x->device));
-    static bool attr_set[64] = {false};
-    if (x->device < 64 && !attr_set[x->device]) {
-        DIOMP_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)GEMM_SMEM));
-        attr_set[x->device] = true;
-    }
     GemmParams p{};
     p.M = x->M; p.N = x->N; p.K = x->K;
     p.A = (const double *)x->A; p.B = (const double *)x->B; p.C = (double *)x->C;
@@ -285,10 +308,12 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
         p.sig_value[i] = x->sig_value[i];
     }
     p.counter = (unsigned int *)x->counter;
-    const int64_t tiles = ceil_div(x->M, BM) * ceil_div(x->N, BN);
-    dgemm_dmma_kernel<<<(unsigned)tiles, GTHREADS, GEMM_SMEM, (cudaStream_t)stream>>>(p);
-    DIOMP_LAUNCH_CHECK();
-    return DIOMP_OK;
+    // default: 2 CTAs/SM with 32x32 warp tiles (0.91 of cuBLAS DGEMM at 8192^3;
+    // the 1-CTA 64x32 and BK=32 variants measured 0.87 / 0.89)
+    const char *v = getenv("DIOMP_DGEMM_CFG");
+    if (v && atoi(v) == 0) return launch_dgemm<CfgBig>(p, x->device, (cudaStream_t)stream);
+    if (v && atoi(v) == 2) return launch_dgemm<CfgDeepK>(p, x->device, (cudaStream_t)stream);
+    return launch_dgemm<CfgDual>(p, x->device, (cudaStream_t)stream);
 }
 
 }  // extern "C"
