@@ -14,7 +14,7 @@ import os
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdiomp_b200.so")
+LIB_PATH = os.environ.get("DIOMP_B200_LIB") or os.path.join(HERE, "libdiomp_b200.so")
 
 MAX_TEAM = 64
 c_u64, c_i64, c_i32, c_u32, c_vp = (ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32,

@@ -46,11 +46,15 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines: list[str] | None = None,
+          out: str | None = None) -> str:
+    """defines/out: experiment builds (e.g. -DDIOMP_STENCIL_NCW=16 into another
+    file, loaded with DIOMP_B200_LIB); the default build is the product."""
+    lib = out or LIB
+    if not force and not defines and lib == LIB and up_to_date():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *NVCC_FLAGS, os.path.join(CSRC, "diomp_b200.cu"), "-o", tmp]
+    tmp = lib + ".tmp"
+    cmd = [NVCC, *NVCC_FLAGS, *(defines or []), os.path.join(CSRC, "diomp_b200.cu"), "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
@@ -58,11 +62,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError(f"nvcc failed (see {log})")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
         sys.stdout.write(res.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose=not defs, defines=defs,
+                out=outs[0] if outs else None))

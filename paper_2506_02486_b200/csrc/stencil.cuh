@@ -36,16 +36,20 @@ namespace diomp {
 namespace stencil {
 
 constexpr int R = 4;
-constexpr int TY = 16;
+#ifndef DIOMP_STENCIL_NCW
+#define DIOMP_STENCIL_NCW 12
+#endif
+constexpr int NCW = DIOMP_STENCIL_NCW;  // compute warps (2 rows each)
+constexpr int TY = 2 * NCW;
 constexpr int TZ = 64;
-constexpr int BY = TY + 2 * R;  // 24 rows per slot
+constexpr int BY = TY + 2 * R;  // rows per slot
 constexpr int BZ = TZ + 2 * R;  // 72 columns per slot
 constexpr int SLOT = BY * BZ;   // doubles per slot
-constexpr int NSLOT = 11;                 // u_cur plane ring: 5 in use + 6 in flight
-constexpr int NPREV = 8;                  // u_prev tile ring
+// smem budget (227 KB): u_cur ring of BY x 72 tiles + u_prev ring of TY x 64 tiles
+constexpr int NSLOT = NCW >= 16 ? 7 : (NCW >= 12 ? 8 : 11);  // 5 in use + the rest in flight
+constexpr int NPREV = NCW >= 16 ? 3 : (NCW >= 12 ? 5 : 8);    // u_prev tile ring
 constexpr int PREV_AHEAD = NPREV - 2;     // u_prev tiles issued this many outputs ahead
 constexpr int PSLOT = TY * TZ;            // doubles per u_prev tile
-constexpr int NCW = 8;                    // compute warps (2 rows each)
 constexpr int THREADS = (NCW + 1) * 32;   // + one TMA producer warp
 constexpr uint32_t SLOT_BYTES = SLOT * 8;
 constexpr uint32_t PSLOT_BYTES = PSLOT * 8;
@@ -301,7 +305,7 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
             for (int pt = 0; pt < 4; ++pt)
                 if (pt == ln.src_pt) out[pt] = __dadd_rn(out[pt], p.amp);
         }
-        store4<FULL>(ln.pn, p.NZ, out, ln);
+        if (!(ln.cache & 16)) store4<FULL>(ln.pn, p.NZ, out, ln);  // bit4: diagnostic no-store
         if (ln.pl && ln.x < 2 * R) store4<FULL>(ln.pl, p.NZ, out, ln);
         if (ln.pr && ln.x >= p.nxl) store4<FULL>(ln.pr, p.NZ, out, ln);
         const int64_t pstride = p.NY * p.NZ;

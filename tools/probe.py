@@ -73,7 +73,23 @@ def stencil(g=512):
             "GBps_24B": 24 * g ** 3 / ms / 1e6}
 
 
+def triad(n_gb=8):
+    """STREAM-style reference for the stencil's access pattern: c = a + b
+    (2 reads + 1 write = 24 B per f64 element) with torch's own kernel."""
+    import torch
+    n = int(n_gb * 2**30 // 8)
+    a = torch.rand(n, dtype=torch.float64, device="cuda")
+    b = torch.rand(n, dtype=torch.float64, device="cuda")
+    c = torch.empty_like(a)
+    ms = _time(lambda: torch.add(a, b, out=c), iters=10)
+    ms_copy = _time(lambda: c.copy_(a), iters=10)
+    ms_read = _time(lambda: a.sum(), iters=10)
+    return {"probe": "triad", "elements": n, "triad_ms": ms, "triad_GBps": 24 * n / ms / 1e6,
+            "copy_GBps": 16 * n / ms_copy / 1e6, "read_GBps": 8 * n / ms_read / 1e6}
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     arg = [int(x) for x in sys.argv[2:]]
-    print(json.dumps({"dgemm": dgemm, "copy": copy, "stencil": stencil}[what](*arg)), flush=True)
+    print(json.dumps({"dgemm": dgemm, "copy": copy, "stencil": stencil, "triad": triad}[what](*arg)),
+          flush=True)
