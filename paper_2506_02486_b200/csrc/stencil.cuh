@@ -46,8 +46,14 @@ constexpr int BY = TY + 2 * R;  // rows per slot
 constexpr int BZ = TZ + 2 * R;  // 72 columns per slot
 constexpr int SLOT = BY * BZ;   // doubles per slot
 // smem budget (227 KB): u_cur ring of BY x 72 tiles + u_prev ring of TY x 64 tiles
-constexpr int NSLOT = NCW >= 16 ? 7 : (NCW >= 12 ? 8 : 11);  // 5 in use + the rest in flight
-constexpr int NPREV = NCW >= 16 ? 3 : (NCW >= 12 ? 5 : 8);    // u_prev tile ring
+#ifndef DIOMP_STENCIL_NSLOT
+#define DIOMP_STENCIL_NSLOT (NCW >= 16 ? 7 : (NCW >= 14 ? 7 : (NCW >= 12 ? 8 : 11)))
+#endif
+#ifndef DIOMP_STENCIL_NPREV
+#define DIOMP_STENCIL_NPREV (NCW >= 16 ? 3 : (NCW >= 14 ? 4 : (NCW >= 12 ? 5 : 8)))
+#endif
+constexpr int NSLOT = DIOMP_STENCIL_NSLOT;  // 5 in use + the rest in flight
+constexpr int NPREV = DIOMP_STENCIL_NPREV;  // u_prev tile ring
 constexpr int PREV_AHEAD = NPREV - 2;     // u_prev tiles issued this many outputs ahead
 constexpr int PSLOT = TY * TZ;            // doubles per u_prev tile
 constexpr int THREADS = (NCW + 1) * 32;   // + one TMA producer warp
