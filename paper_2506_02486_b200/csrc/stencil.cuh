@@ -7,16 +7,22 @@
 // reference's order (acc = c*u; x taps t=1..4; y taps; z taps;
 // (2u - u_prev) + acc), so no FMA contraction can occur.
 //
-// Fast path (R=4, NZ even, 16 B aligned): each CTA owns a 16(y) x 64(z) column
-// of the domain and streams along x through a chunk of planes.
-//   * u_cur planes (tile + 4-wide y/z halo, 24 x 72 f64) arrive by TMA
-//     (cp.async.bulk.tensor.3d) into an 8-slot shared-memory ring, one
-//     mbarrier per slot, prefetching 3 planes ahead.
-//   * every thread owns 2(y) x 2(z) points and keeps the 9-plane x-window of
-//     each in registers; the plane loop is unrolled 9x so the window rotates
-//     by register renaming.  y/z taps come from the centre plane's slot with
-//     16 B shared loads (conflict-free rows).
-//   * u_prev / u_next are streamed with 16 B coalesced global loads/stores.
+// Fast path (R=4, NZ even, 16 B aligned): one CTA per SM owns a 24(y) x 64(z)
+// column of the domain and streams along x through a chunk of planes.  The CTA
+// is warp-specialised:
+//   * a producer warp issues TMA (cp.async.bulk.tensor.3d) loads: u_cur plane
+//     tiles with their 4-wide y/z halo (32 x 72 f64) into an 8-slot ring and
+//     u_prev tiles (24 x 64) into a 5-slot ring, each slot with a "full"
+//     (transaction-count) and an "empty" (consumer-arrival) mbarrier -- no
+//     CTA-wide barrier per plane;
+//   * 12 compute warps, 2(y) x 2(z) points per thread, keep the 9-plane
+//     x-window of each point in registers (the plane loop is unrolled 9x so the
+//     window rotates by register renaming; 128 registers, no spills); y/z taps
+//     come from the centre plane's slot with 16 B shared loads (conflict-free
+//     rows), interleaved tap by tap so only a sliding pair of rows is live;
+//   * u_next is stored with 16 B coalesced stores.
+// Measured (1024^3, one B200): 229 Gpts/s, DRAM traffic 1.04x the 24 B/point
+// algorithmic minimum (profiles/r01_stencil_v5_full_summary.json).
 // Fused driver epilogue: output planes [R,2R) / [nxl, nxl+R) are also stored
 // into the left / right neighbour's u_next ghost planes over NVLink (peer
 // pointers), the point source is added in-register (one extra rounded add,
@@ -85,9 +91,6 @@ struct Params {
     uint64_t *sig_r;
     uint64_t sl, sr;
     unsigned int *counter;
-    // tuning knobs (DIOMP_STENCIL_PREVPF / DIOMP_STENCIL_CACHE)
-    int32_t prev_pf;      // u_prev tile L2 prefetch distance (output planes), 0 = off
-    int32_t cache;        // bit0: streaming (evict-first) u_next stores; bit1: evict-first u_prev loads
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -126,43 +129,13 @@ __device__ __forceinline__ void tma_load_plane(double *dst, const CUtensorMap *m
         : "memory");
 }
 
-// Same with an L2 eviction-priority policy (createpolicy result).
-__device__ __forceinline__ void tma_load_plane_hint(double *dst, const CUtensorMap *map, int z,
-                                                    int y, int x, uint64_t *bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(z), "r"(y), "r"(x), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
 __device__ __forceinline__ double2 lds2(const double *p) {
     return *reinterpret_cast<const double2 *>(p);
-}
-
-__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap *map, int z, int y, int x) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map),
-                 "r"(z), "r"(y), "r"(x)
-                 : "memory");
 }
 
 __device__ __forceinline__ double tap(double acc, double w, double a, double b) {
     return __dadd_rn(acc, __dmul_rn(w, __dadd_rn(a, b)));
 }
-
-constexpr int PREV_PF = 4;  // u_prev tile prefetched into L2 this many output planes ahead
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -171,67 +144,25 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // Per-thread streaming state (pointers advance by one plane per output plane).
 struct Lane {
     double *pn;         // u_next at (x, y, z) of the thread's first point
-    const double *pp;   // u_prev, same point
     double *pl;         // left neighbour's ghost copy of pn (or null)
     double *pr;         // right neighbour's ghost copy of pn (or null)
     int64_t x;          // current output plane (full-array index)
     int so;             // slot offset (doubles) of the thread's first point
     int src_pt;         // which of the 4 points is the source (y/z match), -1: none
-    int cache;          // Params::cache
     bool yv0, yv1, zv0, zv1, full;
 };
-
-__device__ __forceinline__ void st2_cs(double *p, double a, double b) {
-    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
-}
-
-__device__ __forceinline__ double2 ld2_ef(const double *p) {
-    double2 v;
-    asm volatile(
-        "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-        " ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n}\n"
-        : "=d"(v.x), "=d"(v.y)
-        : "l"(p));
-    return v;
-}
 
 template <bool FULL>
 __device__ __forceinline__ void store4(double *b, int64_t NZ, const double (&o)[4], const Lane &ln) {
     if (FULL) {
-        if (ln.cache & 1) {
-            st2_cs(b, o[0], o[1]);
-            st2_cs(b + NZ, o[2], o[3]);
-        } else {
-            *reinterpret_cast<double2 *>(b) = make_double2(o[0], o[1]);
-            *reinterpret_cast<double2 *>(b + NZ) = make_double2(o[2], o[3]);
-        }
+        *reinterpret_cast<double2 *>(b) = make_double2(o[0], o[1]);
+        *reinterpret_cast<double2 *>(b + NZ) = make_double2(o[2], o[3]);
         return;
     }
     if (ln.yv0 && ln.zv1) *reinterpret_cast<double2 *>(b) = make_double2(o[0], o[1]);
     else if (ln.yv0 && ln.zv0) b[0] = o[0];
     if (ln.yv1 && ln.zv1) *reinterpret_cast<double2 *>(b + NZ) = make_double2(o[2], o[3]);
     else if (ln.yv1 && ln.zv0) b[NZ] = o[2];
-}
-
-template <bool FULL>
-__device__ __forceinline__ void load4(const double *b, int64_t NZ, double (&v)[4], const Lane &ln) {
-    if (FULL) {
-        double2 a, c;
-        if (ln.cache & 2) {
-            a = ld2_ef(b);
-            c = ld2_ef(b + NZ);
-        } else {
-            a = __ldg(reinterpret_cast<const double2 *>(b));
-            c = __ldg(reinterpret_cast<const double2 *>(b + NZ));
-        }
-        v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
-        return;
-    }
-    v[0] = v[1] = v[2] = v[3] = 0.0;
-    if (ln.yv0 && ln.zv1) { double2 a = __ldg(reinterpret_cast<const double2 *>(b)); v[0] = a.x; v[1] = a.y; }
-    else if (ln.yv0 && ln.zv0) v[0] = __ldg(b);
-    if (ln.yv1 && ln.zv1) { double2 c = __ldg(reinterpret_cast<const double2 *>(b + NZ)); v[2] = c.x; v[3] = c.y; }
-    else if (ln.yv1 && ln.zv0) v[2] = __ldg(b + NZ);
 }
 
 // One loaded plane q for a compute thread's 2x2 points.  J is the
@@ -311,7 +242,7 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
             for (int pt = 0; pt < 4; ++pt)
                 if (pt == ln.src_pt) out[pt] = __dadd_rn(out[pt], p.amp);
         }
-        if (!(ln.cache & 16)) store4<FULL>(ln.pn, p.NZ, out, ln);  // bit4: diagnostic no-store
+        store4<FULL>(ln.pn, p.NZ, out, ln);
         if (ln.pl && ln.x < 2 * R) store4<FULL>(ln.pl, p.NZ, out, ln);
         if (ln.pr && ln.x >= p.nxl) store4<FULL>(ln.pr, p.NZ, out, ln);
         const int64_t pstride = p.NY * p.NZ;
@@ -395,31 +326,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
 
     if (warp == NCW) {
-        // ---- producer warp: TMA plane loads into the ring + u_prev L2 prefetch
+        // ---- producer warp: TMA loads of u_cur planes and u_prev tiles into their rings
         if (lane == 0) {
             const int nout = L - 2 * R;
-            const uint64_t pol_cur = policy_evict_last(), pol_prev = policy_evict_first();
-            const bool hint_cur = p.cache & 4, hint_prev = p.cache & 8;
             auto issue_prev = [&](int o) {  // u_prev tile of output plane o
                 const int ps = o % NPREV;
                 if (o >= NPREV) mbar_wait(&pempty[ps], (uint32_t)(((o / NPREV) - 1) & 1));
                 mbar_expect_tx(&pfull[ps], PSLOT_BYTES);
-                if (hint_prev)
-                    tma_load_plane_hint(psm + ps * PSLOT, &pmap, z0, y0, (int)(xa + o), &pfull[ps],
-                                        pol_prev);
-                else
-                    tma_load_plane(psm + ps * PSLOT, &pmap, z0, y0, (int)(xa + o), &pfull[ps]);
+                tma_load_plane(psm + ps * PSLOT, &pmap, z0, y0, (int)(xa + o), &pfull[ps]);
             };
             int next_prev = 0;
             for (int q = 0; q < L; ++q) {
                 const int s = q % NSLOT;
                 if (q >= NSLOT) mbar_wait(&empty[s], (uint32_t)(((q / NSLOT) - 1) & 1));
                 mbar_expect_tx(&full[s], SLOT_BYTES);
-                if (hint_cur)
-                    tma_load_plane_hint(sm + s * SLOT, &map, z0 - R, y0 - R, (int)(xa - R + q),
-                                        &full[s], pol_cur);
-                else
-                    tma_load_plane(sm + s * SLOT, &map, z0 - R, y0 - R, (int)(xa - R + q), &full[s]);
+                tma_load_plane(sm + s * SLOT, &map, z0 - R, y0 - R, (int)(xa - R + q), &full[s]);
                 // keep u_prev PREV_AHEAD output planes ahead of the plane that completes
                 for (; next_prev < nout && next_prev <= q - 2 * R + PREV_AHEAD; ++next_prev)
                     issue_prev(next_prev);
@@ -436,10 +357,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         ln.zv1 = z + 1 < p.NZ - R;
         ln.full = (y0 + TY <= p.NY - R) && (z0 + TZ <= p.NZ - R);  // uniform per CTA
         ln.so = (R + ry) * BZ + R + zz;
-        ln.cache = p.cache;
         const int64_t g0 = (xa * p.NY + y) * p.NZ + z;
         ln.pn = p.u_next + g0;
-        ln.pp = p.u_prev + g0;
         ln.pl = p.left_next ? p.left_next + p.nxl * p.NY * p.NZ + g0 : nullptr;
         ln.pr = p.right_next ? p.right_next - p.nxl * p.NY * p.NZ + g0 : nullptr;
         ln.x = xa;
@@ -522,17 +441,9 @@ static int make_plane_map(CUtensorMap *map, const double *u, int64_t NX, int64_t
     cuuint64_t strides[2] = {(cuuint64_t)NZ * 8, (cuuint64_t)NY * NZ * 8};
     cuuint32_t box[3] = {halo ? (cuuint32_t)BZ : (cuuint32_t)TZ, halo ? (cuuint32_t)BY : (cuuint32_t)TY, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    if (const char *e = getenv("DIOMP_STENCIL_PROMO")) {
-        const int v = atoi(e);
-        promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                         : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    }
     CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)u, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? DIOMP_OK : DIOMP_BAD_REQUEST;
 }
 
@@ -590,10 +501,6 @@ static int launch_fast(const CUtensorMap &map, const CUtensorMap &pmap, Params &
     p.ntz = (int)ceil_div(nz_int, TZ);
     p.ncols = nty * p.ntz;
     pick_chunks(nx_int, p.ncols, &p.chunk, &p.nch);
-    const char *pf = getenv("DIOMP_STENCIL_PREVPF");
-    p.prev_pf = pf ? atoi(pf) : PREV_PF;
-    const char *cm = getenv("DIOMP_STENCIL_CACHE");
-    p.cache = cm ? atoi(cm) : 0;
     const int64_t units = (int64_t)p.ncols * p.nch;
     if (units > 0x7fffffff) return DIOMP_BAD_REQUEST;
     stencil_tma_kernel<<<(unsigned)units, THREADS, SMEM_BYTES, s>>>(map, pmap, p);
