@@ -108,3 +108,12 @@ def test_allocator_restatements_match_reference_traces():
                 except MemoryError:
                     trace.append(["oom"])
         assert trace == gold[name]["trace"], name
+
+
+def test_full_size_golden_recorded_with_provenance():
+    """1024^3 x 3 steps: the reference's checksum was reproduced by
+    the C oracle in 63 s when the fixture was recorded; the GPU suite checks the
+    CUDA path against it (tests/test_gpu_edges.py)."""
+    full = GOLD["full_size"][0]
+    assert (full["nx"], full["steps"]) == (1024, 3)
+    assert full["sha256"].startswith("3277fbcc")
