@@ -26,8 +26,10 @@ def _store_timeout(seconds: float):
 class ControlPlane:
     """Tagged point-to-point messages over a key-value store.
 
-    Keys are consumed (deleted) by the receiver, so a tag may be reused as
-    soon as the previous message with that tag was received.
+    Every (tag, src, dst) stream is FIFO: the key carries a per-stream
+    sequence number kept on both sides, so a sender that runs ahead never
+    overwrites a message its receiver has not consumed yet.  Keys are deleted
+    by the receiver.
     """
 
     def __init__(self, store, rank: int, nranks: int, timeout: float = 60.0, prefix: str = "d"):
@@ -38,17 +40,26 @@ class ControlPlane:
         self.prefix = prefix
         self._lock = threading.Lock()
         self._seq: dict = {}
+        self._sent: dict = {}
+        self._recvd: dict = {}
 
     # -- raw messaging ---------------------------------------------------------
-    def _key(self, tag, src: int, dst: int) -> str:
+    def _key(self, tag, src: int, dst: int, n: int) -> str:
         t = tag.decode() if isinstance(tag, bytes) else str(tag)
-        return f"{self.prefix}/m/{t}/{src}>{dst}"
+        return f"{self.prefix}/m/{t}/{src}>{dst}#{n}"
+
+    def _bump(self, table: dict, k) -> int:
+        with self._lock:
+            n = table.get(k, 0)
+            table[k] = n + 1
+            return n
 
     def send(self, dst: int, tag, blob: bytes):
-        self.store.set(self._key(tag, self.rank, dst), blob)
+        n = self._bump(self._sent, (tag, dst))
+        self.store.set(self._key(tag, self.rank, dst, n), blob)
 
     def recv(self, tag, src: int, timeout: float | None = None) -> bytes:
-        key = self._key(tag, src, self.rank)
+        key = self._key(tag, src, self.rank, self._bump(self._recvd, (tag, src)))
         try:
             self.store.wait([key], _store_timeout(timeout or self.timeout))
         except Exception as e:  # torch raises DistStoreError / RuntimeError
