@@ -83,6 +83,8 @@ int diomp_event_sync(void *event);
 int diomp_event_destroy(void *event);
 int diomp_event_elapsed_ms(void *start, void *stop, float *ms_out);
 int diomp_stream_wait_event(void *stream, void *event);
+int diomp_stream_query(void *stream); /* DIOMP_OK idle, DIOMP_PENDING busy */
+
 
 /* ---- one-sided data plane: runtime.py:371-470 (put/get) replacing
  *      transport.py:508-566 (rma_put/rma_get frames).  D2D transfers are an

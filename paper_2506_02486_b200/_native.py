@@ -89,6 +89,7 @@ _PROTOS = {
     "diomp_event_destroy": [c_vp],
     "diomp_event_elapsed_ms": [c_vp, c_vp, ctypes.POINTER(ctypes.c_float)],
     "diomp_stream_wait_event": [c_vp, c_vp],
+    "diomp_stream_query": [c_vp],
     "diomp_copy": [ctypes.c_int, c_u64, c_u64, c_u64, c_vp],
     "diomp_memcpy_async": [c_u64, c_u64, c_u64, ctypes.c_int, c_vp],
     "diomp_memset_async": [c_u64, ctypes.c_int, c_u64, c_vp],

@@ -7,6 +7,8 @@
 // NVLink directly -- no frames, no progress thread.
 #pragma once
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace diomp {
@@ -300,6 +302,16 @@ int diomp_stream_wait_event(void *stream, void *event) {
     return DIOMP_OK;
 }
 
+int diomp_stream_query(void *stream) {
+    cudaError_t e = cudaStreamQuery((cudaStream_t)stream);
+    if (e == cudaSuccess) return DIOMP_OK;
+    if (e == cudaErrorNotReady) {
+        cudaGetLastError();
+        return DIOMP_PENDING;
+    }
+    return DIOMP_CUDA_ERROR_BASE + (int)e;
+}
+
 // ---- data plane ---------------------------------------------------------------
 
 int diomp_copy(int device, uint64_t dst, uint64_t src, uint64_t nbytes, void *stream) {
@@ -328,6 +340,10 @@ int diomp_memcpy_sync(int device, uint64_t dst, uint64_t src, uint64_t nbytes, i
     DIOMP_CUDA_TRY(cudaSetDevice(device));
     DIOMP_CUDA_TRY(cudaDeviceSynchronize());
     DIOMP_CUDA_TRY(cudaMemcpy((void *)dst, (const void *)src, nbytes, cudaMemcpyDefault));
+    // A pageable H2D cudaMemcpy may return once the bytes are staged, before
+    // the DMA lands; work on other (non-blocking) streams is not ordered
+    // after it, so drain the device before reporting the write done.
+    DIOMP_CUDA_TRY(cudaDeviceSynchronize());
     return DIOMP_OK;
 }
 

@@ -93,8 +93,11 @@ def test_asymmetric_two_step_access_and_checks():
             back = bytearray(len(payload))
             rt.get(addr, back, len(payload), d.TransferKind.D2H).wait()
             assert bytes(back) == payload
-            with pytest.raises(d.InvalidAddress):              # beyond rank 1's payload
-                rt.put(d.GlobalAddress(1, 0, addr.offset + 8192), b"x" * 64, 64,
+            with pytest.raises(d.InvalidAddress):              # straddles its end
+                rt.put(d.GlobalAddress(1, 0, addr.offset + 8192 - 32), b"x" * 64, 64,
+                       d.TransferKind.H2D)
+            with pytest.raises(d.InvalidAddress):              # below its start
+                rt.put(d.GlobalAddress(1, 0, addr.offset - 64), b"x" * 64, 64,
                        d.TransferKind.H2D)
         rt.barrier(rt.world)
         return True
