@@ -44,7 +44,9 @@ int diomp_device_sync(int device);
 /* Device-side wait timeouts (see diomp_wait) are recorded, not trapped:
  * returns DIOMP_INTERNAL (and clears it) if any wait on `device` timed out. */
 int diomp_device_error(int device);
-int diomp_set_wait_timeout(int device, double seconds); /* default 30 s */
+/* Sets the device wait timeout (default 30 s) and maps a pinned mirror of the
+ * error word, after which diomp_device_error is a host load, not a CUDA call. */
+int diomp_set_wait_timeout(int device, double seconds);
 
 /* ---- segments: global_memory.py:190-206 (GlobalMemory.__init__ arenas),
  *      segment_create global_memory.py:391-393.  A segment is one zero-filled
@@ -77,6 +79,7 @@ int diomp_stream_create(int device, void **stream_out);
 int diomp_stream_destroy(void *stream);
 int diomp_stream_sync(void *stream);
 int diomp_event_create(int device, void **event_out);
+int diomp_event_create_sync(int device, void **event_out); /* no timing: cheaper record */
 int diomp_event_record(void *event, void *stream);
 int diomp_event_query(void *event); /* DIOMP_OK when complete, DIOMP_PENDING otherwise */
 int diomp_event_sync(void *event);

@@ -83,6 +83,7 @@ _PROTOS = {
     "diomp_stream_destroy": [c_vp],
     "diomp_stream_sync": [c_vp],
     "diomp_event_create": [ctypes.c_int, ctypes.POINTER(c_vp)],
+    "diomp_event_create_sync": [ctypes.c_int, ctypes.POINTER(c_vp)],
     "diomp_event_record": [c_vp, c_vp],
     "diomp_event_query": [c_vp],
     "diomp_event_sync": [c_vp],
@@ -175,9 +176,9 @@ def stream_create(device: int) -> int:
     return out.value or 0
 
 
-def event_create(device: int) -> int:
+def event_create(device: int, timing: bool = True) -> int:
     out = c_vp()
-    call("diomp_event_create", device, ctypes.byref(out))
+    call("diomp_event_create" if timing else "diomp_event_create_sync", device, ctypes.byref(out))
     return out.value
 
 

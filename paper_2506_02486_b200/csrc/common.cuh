@@ -29,6 +29,19 @@ constexpr int kNumSMs = 148;
 // are plain definitions.
 __device__ unsigned int g_device_error = 0;
 __device__ unsigned long long g_wait_timeout_ns = 30ull * 1000 * 1000 * 1000;
+// Optional pinned, device-mapped mirror of the error word (set up by
+// diomp_set_wait_timeout): the host then polls it with a plain load instead
+// of a synchronous cudaMemcpyFromSymbol after every fence.
+__device__ unsigned int *g_error_word = nullptr;
+
+__device__ __forceinline__ void record_device_error(unsigned int code) {
+    atomicExch(&g_device_error, code);
+    unsigned int *w = g_error_word;
+    if (w) {
+        *(volatile unsigned int *)w = code;
+        __threadfence_system();
+    }
+}
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
     uint64_t t;
@@ -56,7 +69,7 @@ __device__ __forceinline__ bool wait_ge(const uint64_t *flag, uint64_t value) {
         __nanosleep(ns);
         if (ns < 1024) ns <<= 1;
         if (globaltimer_ns() - t0 > limit) {
-            atomicExch(&g_device_error, (unsigned)DIOMP_INTERNAL);
+            record_device_error((unsigned)DIOMP_INTERNAL);
             return false;
         }
     }

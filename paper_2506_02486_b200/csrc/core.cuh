@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstring>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -161,7 +162,32 @@ int diomp_device_sync(int device) {
     return DIOMP_OK;
 }
 
+static unsigned int *g_host_error_word[64] = {};
+static std::mutex g_error_word_mu;
+
+static int ensure_error_word(int device) {
+    if (device < 0 || device >= 64) return DIOMP_OK;
+    std::lock_guard<std::mutex> lk(g_error_word_mu);
+    if (g_host_error_word[device]) return DIOMP_OK;
+    void *p = nullptr, *dp = nullptr;
+    DIOMP_CUDA_TRY(cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(p, 0, 64);
+    DIOMP_CUDA_TRY(cudaHostGetDevicePointer(&dp, p, 0));
+    DIOMP_CUDA_TRY(cudaMemcpyToSymbol(g_error_word, &dp, sizeof(dp)));
+    g_host_error_word[device] = (unsigned int *)p;
+    return DIOMP_OK;
+}
+
 int diomp_device_error(int device) {
+    unsigned int *w = (device >= 0 && device < 64) ? g_host_error_word[device] : nullptr;
+    if (w) {  // mapped mirror: no CUDA call unless an error was recorded
+        unsigned int err = __atomic_exchange_n(w, 0u, __ATOMIC_ACQ_REL);
+        if (!err) return DIOMP_OK;
+        unsigned int zero = 0;
+        DIOMP_CUDA_TRY(cudaSetDevice(device));
+        DIOMP_CUDA_TRY(cudaMemcpyToSymbol(g_device_error, &zero, sizeof(zero)));
+        return (int)err;
+    }
     DIOMP_CUDA_TRY(cudaSetDevice(device));
     unsigned int err = 0, zero = 0;
     DIOMP_CUDA_TRY(cudaMemcpyFromSymbol(&err, g_device_error, sizeof(err)));
@@ -171,6 +197,8 @@ int diomp_device_error(int device) {
 
 int diomp_set_wait_timeout(int device, double seconds) {
     DIOMP_CUDA_TRY(cudaSetDevice(device));
+    int rc = ensure_error_word(device);
+    if (rc) return rc;
     unsigned long long ns = (unsigned long long)(seconds * 1e9);
     DIOMP_CUDA_TRY(cudaMemcpyToSymbol(g_wait_timeout_ns, &ns, sizeof(ns)));
     return DIOMP_OK;
@@ -263,6 +291,14 @@ int diomp_event_create(int device, void **event_out) {
     DIOMP_CUDA_TRY(cudaSetDevice(device));
     cudaEvent_t e;
     DIOMP_CUDA_TRY(cudaEventCreate(&e));
+    *event_out = (void *)e;
+    return DIOMP_OK;
+}
+
+int diomp_event_create_sync(int device, void **event_out) {
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    cudaEvent_t e;
+    DIOMP_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     *event_out = (void *)e;
     return DIOMP_OK;
 }
