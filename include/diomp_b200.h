@@ -95,6 +95,13 @@ int diomp_stream_query(void *stream); /* DIOMP_OK idle, DIOMP_PENDING busy */
  *      stores cross NVLink; get: the destination's device, loads cross
  *      NVLink).  dst/src may be peer-mapped addresses.                       */
 int diomp_copy(int device, uint64_t dst, uint64_t src, uint64_t nbytes, void *stream);
+/* Runtime.put / Runtime.get D2D legs (runtime.py:371-419 / 421-470).  `remote`
+ * = the far side is another GPU.  Engine per size (DIOMP_PUT_ENGINE /
+ * DIOMP_GET_ENGINE override): remote put >= 64 KiB on the copy engine (SM
+ * stores to a peer cap at ~715 GB/s, CE reaches 779), remote get >= 16 MiB on
+ * the bulk-async TMA kernel, everything else on the SM copy kernel.          */
+int diomp_put(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int remote, void *stream);
+int diomp_get(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int remote, void *stream);
 /* host<->device legs of H2D put / D2H get (TransferKind, global_memory.py:52-70) */
 #define DIOMP_H2D 1
 #define DIOMP_D2H 2
@@ -118,7 +125,8 @@ int diomp_wait(int device, uint64_t flag_addr, uint64_t value, void *stream);
  * slot[q] (the global endpoint index of the signalling position q).
  * epoch_to[q] / epoch_from[q]: signals already sent to / received from q on
  * this pair; an entry+exit synchronised call consumes two (+1 entry, +2 exit)
- * and the caller advances both by 2 afterwards.  sync=0 skips all flag
+ * and the caller advances both by 2 afterwards -- allreduce consumes three
+ * (+1 entry, +2 phase, +3 exit) on both of its algorithms.  sync=0 skips all flag
  * traffic (the caller orders the endpoints with host barriers; used when
  * several endpoints share one GPU).                                           */
 typedef struct {
@@ -140,7 +148,11 @@ int diomp_team_barrier(const diomp_team *team, void *stream);
  *      (same on every position).  Results are bit-identical to the
  *      reference's ring folds:
  *        reduce:    root gets ((v_root op v_root+1) op ...) op v_root-1
- *        allreduce: block b=[b*count/k,(b+1)*count/k) folded from position b. */
+ *        allreduce: block b=[b*count/k,(b+1)*count/k) folded from position b.
+ * allreduce is one kernel (fold, store the block to every member); from
+ * diomp_set_allreduce_ce_min() bytes (default never; DIOMP_AR_ALGO=ce: all)
+ * the fold goes to the own recv and the copy engine pushes it to the peers.
+ * Same bits either way.                                                      */
 #define DIOMP_F32 0
 #define DIOMP_F64 1
 #define DIOMP_I32 2
@@ -152,6 +164,7 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
                 void *stream);
 int diomp_reduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
                  int32_t dtype, int32_t op, int32_t root, void *stream);
+int diomp_set_allreduce_ce_min(uint64_t bytes);
 int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off,
                     uint64_t count, int32_t dtype, int32_t op, void *stream);
 

@@ -92,6 +92,8 @@ _PROTOS = {
     "diomp_stream_wait_event": [c_vp, c_vp],
     "diomp_stream_query": [c_vp],
     "diomp_copy": [ctypes.c_int, c_u64, c_u64, c_u64, c_vp],
+    "diomp_put": [ctypes.c_int, c_u64, c_u64, c_u64, ctypes.c_int, c_vp],
+    "diomp_get": [ctypes.c_int, c_u64, c_u64, c_u64, ctypes.c_int, c_vp],
     "diomp_memcpy_async": [c_u64, c_u64, c_u64, ctypes.c_int, c_vp],
     "diomp_memset_async": [c_u64, ctypes.c_int, c_u64, c_vp],
     "diomp_memcpy_sync": [ctypes.c_int, c_u64, c_u64, c_u64, ctypes.c_int],
@@ -100,6 +102,7 @@ _PROTOS = {
     "diomp_team_barrier": [ctypes.POINTER(Team), c_vp],
     "diomp_bcast": [ctypes.POINTER(Team), c_u64, c_u64, c_i32, c_vp],
     "diomp_reduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_i32, c_vp],
+    "diomp_set_allreduce_ce_min": [c_u64],
     "diomp_allreduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_vp],
     "diomp_stencil_update": [ctypes.c_int, ctypes.POINTER(StencilArgs), c_vp],
     "diomp_stencil_run": [ctypes.POINTER(StencilPlan), c_i64, c_i64, c_vp],

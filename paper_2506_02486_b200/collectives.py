@@ -165,8 +165,10 @@ def _after_torch(rt: Runtime, device: int):
     torch.cuda.current_stream(gpu).synchronize()
 
 
-def _run(comm: Communicator, launch, blocking: bool = True):
+def _run(comm: Communicator, launch, blocking: bool = True, signals: int = 2):
     """launch(team, stream) for every local position, device- or host-synchronised.
+    `signals` = device signals the call consumes per ordered pair (allreduce 3:
+    entry, phase, exit; reduce / bcast 2: entry, exit).
     blocking=False (device-synchronised rings only) enqueues and returns: the
     result is ready once the rank's RMA stream of that device has drained."""
     rt = comm.rt
@@ -194,7 +196,7 @@ def _run(comm: Communicator, launch, blocking: bool = True):
             me = rt.endpoint_index(me_ep.rank, me_ep.device)
             for q, ep in enumerate(comm.ring):
                 if q != pos:
-                    rt.advance_pair(me, rt.endpoint_index(ep.rank, ep.device), 2)
+                    rt.advance_pair(me, rt.endpoint_index(ep.rank, ep.device), signals)
     elif comm.size > 1:
         rt.barrier(comm.group)
 
@@ -283,7 +285,8 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
         return
     comm._next_seq()
     _run(comm, lambda t, s: _native.lib.diomp_allreduce(t, send.offset, recv.offset, count,
-                                                        op.etype.code, op.code, s), blocking)
+                                                        op.etype.code, op.code, s), blocking,
+         signals=3)
 
 
 def device_bcast(rt: Runtime, var: GlobalAddress, nbytes: int, group: Group):

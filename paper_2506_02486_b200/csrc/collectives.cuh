@@ -21,6 +21,11 @@
 // cross-collective slot race of the reference cannot occur.
 #pragma once
 
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace diomp {
@@ -102,13 +107,16 @@ __device__ __forceinline__ void entry_barrier(const diomp_team &t) {
     __syncthreads();
 }
 
-__device__ __forceinline__ void exit_barrier(const diomp_team &t) {
+// Exit: the last CTA signals epoch+`e` to every peer and waits for theirs.
+// Allreduce consumes three signals per call (entry, phase, exit) on both of
+// its paths, reduce and bcast two.
+__device__ __forceinline__ void exit_barrier(const diomp_team &t, int e = 2) {
     if (!t.sync) return;
     if (last_cta_done((unsigned int *)(t.base[t.pos] + t.counter_off), gridDim.x)) {
         const int q = threadIdx.x;
         if (q < t.k && q != t.pos) {
-            st_release_sys((uint64_t *)(t.base[q] + t.flag_off) + t.slot[t.pos], t.epoch_to[q] + 2);
-            wait_ge((const uint64_t *)(t.base[t.pos] + t.flag_off) + t.slot[q], t.epoch_from[q] + 2);
+            st_release_sys((uint64_t *)(t.base[q] + t.flag_off) + t.slot[t.pos], t.epoch_to[q] + e);
+            wait_ge((const uint64_t *)(t.base[t.pos] + t.flag_off) + t.slot[q], t.epoch_from[q] + e);
         }
     }
 }
@@ -134,16 +142,20 @@ __device__ __forceinline__ void fold_range(const Args &a, uint64_t lo, uint64_t 
     }
     auto src = [&](int p) { return (const T *)(t.base[p] + a.send_off); };
     auto dst = [&](int p) { return (T *)(t.base[p] + a.recv_off); };
-    // vector body
+    // vector body: element vlo sits on a 16-byte boundary in every member's
+    // send and recv buffer (same offsets, same alignment)
     using VT = uint4;
-    for (uint64_t v = vlo / V + gtid; v < vhi / V; v += gsz) {
+    auto vsrc = [&](int p) { return reinterpret_cast<const VT *>(src(p) + vlo); };
+    auto vdst = [&](int p) { return reinterpret_cast<VT *>(dst(p) + vlo); };
+    const uint64_t nvec = (vhi - vlo) / V;
+    for (uint64_t v = gtid; v < nvec; v += gsz) {
         VT buf[KMAX];
 #pragma unroll
         for (int i = 0; i < KMAX; ++i)
             if (i < k) {
                 int pidx = start + i;
                 if (pidx >= k) pidx -= k;
-                buf[i] = reinterpret_cast<const VT *>(src(pidx))[v];
+                buf[i] = vsrc(pidx)[v];
             }
         T acc[V];
         const T *b0 = reinterpret_cast<const T *>(&buf[0]);
@@ -158,12 +170,12 @@ __device__ __forceinline__ void fold_range(const Args &a, uint64_t lo, uint64_t 
             }
         VT out = *reinterpret_cast<VT *>(acc);
         if (only >= 0) {
-            reinterpret_cast<VT *>(dst(only))[v] = out;
+            vdst(only)[v] = out;
         } else {
             for (int i = 0; i < k; ++i) {
                 int pidx = t.pos + i;  // own copy first, then peers
                 if (pidx >= k) pidx -= k;
-                reinterpret_cast<VT *>(dst(pidx))[v] = out;
+                vdst(pidx)[v] = out;
             }
         }
     }
@@ -183,15 +195,30 @@ __device__ __forceinline__ void fold_range(const Args &a, uint64_t lo, uint64_t 
     }
 }
 
+// mode 0: fused allreduce (fold block p, store it to every member);
+// mode 1: reduce to the root;
+// mode 2: allreduce step 1 of 3 (fold block p into the own recv only; the
+//         copy engine then pushes it to every peer).
 template <typename T, typename OP, int KMAX>
 __global__ void __launch_bounds__(THREADS) reduce_kernel(const __grid_constant__ Args a) {
     entry_barrier(a.t);
     const int k = a.t.k, p = a.t.pos;
     const uint64_t lo = (uint64_t)p * a.count / k, hi = (uint64_t)(p + 1) * a.count / k;
-    if (a.mode == 0) fold_range<T, OP, KMAX>(a, lo, hi, p, -1);
-    else fold_range<T, OP, KMAX>(a, lo, hi, a.root, a.root);
-    exit_barrier(a.t);
+    if (a.mode == 0) {
+        fold_range<T, OP, KMAX>(a, lo, hi, p, -1);
+        exit_barrier(a.t, 3);
+    } else if (a.mode == 1) {
+        fold_range<T, OP, KMAX>(a, lo, hi, a.root, a.root);
+        exit_barrier(a.t, 2);
+    } else {
+        fold_range<T, OP, KMAX>(a, lo, hi, p, p);
+    }
 }
+
+// Allreduce step 3 of 3 (after the copy-engine pushes of step 2): signal
+// every peer epoch+3 and wait for theirs -- our block has landed in every
+// member's recv and theirs in ours.
+__global__ void allreduce_exit_kernel(const __grid_constant__ Args a) { exit_barrier(a.t, 3); }
 
 // bcast: non-root position p handles block j = (p - root - 1 mod k) of k-1.
 __global__ void __launch_bounds__(THREADS) bcast_kernel(const __grid_constant__ Args a) {
@@ -252,15 +279,52 @@ static int grid_for(uint64_t work_items) {
     return (int)want;
 }
 
+// Allreduce algorithm.  fused (default): one kernel, block p folded from the
+// peers' send buffers (loads) and stored to every member (SM stores).  ce: the
+// same fold into the own recv only, then the copy engine pushes block p to
+// every peer, then an exit barrier.  Measured on 2 B200 (f32 sum, busBW):
+// fused 493 / 617 / 660 GB/s at 64 MiB / 256 MiB / 1 GiB, ce 421 / 522 / 561
+// -- the fold and the push run back to back instead of overlapping, which
+// costs more than the copy engine's better bidirectional write rate (~774 vs
+// ~697 GB/s per direction, profiles/r01_nvlink_probe.txt) gains.  Kept as an
+// option: DIOMP_AR_ALGO=ce or diomp_set_allreduce_ce_min().
+static std::atomic<uint64_t> g_ar_ce_min{~0ull};
+static std::once_flag g_ar_once;
+
+static uint64_t ar_ce_min() {
+    std::call_once(g_ar_once, [] {
+        const char *e = getenv("DIOMP_AR_ALGO");
+        if (e && !strcmp(e, "ce")) g_ar_ce_min = 0;
+    });
+    return g_ar_ce_min.load(std::memory_order_relaxed);
+}
+
 template <typename T, typename OP>
-static int launch_reduce(const Args &a, cudaStream_t s) {
+static int launch_reduce(Args a, cudaStream_t s) {
     const uint64_t per = a.count / a.t.k + 1;
     const uint64_t items = per / (16 / sizeof(T)) + 1;
     const int g = grid_for(items);
+    const bool ce = a.mode == 0 && a.t.sync && a.t.k > 1 && a.count * sizeof(T) >= ar_ce_min();
+    if (ce) a.mode = 2;
     if (a.t.k <= 8) reduce_kernel<T, OP, 8><<<g, THREADS, 0, s>>>(a);
     else if (a.t.k <= 16) reduce_kernel<T, OP, 16><<<g, THREADS, 0, s>>>(a);
     else reduce_kernel<T, OP, DIOMP_MAX_TEAM><<<g, THREADS, 0, s>>>(a);
     DIOMP_LAUNCH_CHECK();
+    if (ce) {
+        const int k = a.t.k, p = a.t.pos;
+        const uint64_t lo = (uint64_t)p * a.count / k * sizeof(T);
+        const uint64_t hi = (uint64_t)(p + 1) * a.count / k * sizeof(T);
+        if (hi > lo) {
+            const uint8_t *src = (const uint8_t *)(a.t.base[p] + a.recv_off) + lo;
+            for (int i = 1; i < k; ++i) {
+                const int q = (p + i) % k;
+                uint8_t *dst = (uint8_t *)(a.t.base[q] + a.recv_off) + lo;
+                DIOMP_CUDA_TRY(cudaMemcpyAsync(dst, src, hi - lo, cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        allreduce_exit_kernel<<<1, 64, 0, s>>>(a);
+        DIOMP_LAUNCH_CHECK();
+    }
     return DIOMP_OK;
 }
 
@@ -292,6 +356,12 @@ static bool team_ok(const diomp_team *t) {
 }  // namespace diomp
 
 extern "C" {
+
+int diomp_set_allreduce_ce_min(uint64_t bytes) {
+    diomp::coll::ar_ce_min();  // settle the environment default first
+    diomp::coll::g_ar_ce_min.store(bytes, std::memory_order_relaxed);
+    return DIOMP_OK;
+}
 
 int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
                     int32_t dtype, int32_t op, void *stream) {

@@ -3,8 +3,10 @@
 // Replaces the reference's simulated arenas (global_memory.py:190-206) and
 // frame transport (transport.py:508-566, 830-861): a segment is one
 // cudaMalloc per device, peers reach it through CUDA IPC or peer access, and
-// put/get are SM-issued copy kernels whose loads (get) or stores (put) cross
-// NVLink directly -- no frames, no progress thread.
+// put/get move bytes over NVLink directly on the initiator's stream -- no
+// frames, no progress thread: SM copy kernels (small transfers, local copies),
+// the copy engine for large remote puts, a bulk-async TMA kernel for large
+// remote gets (see diomp_put / diomp_get for the measured crossovers).
 #pragma once
 
 #include <cstring>
@@ -50,6 +52,91 @@ __global__ void copy8_kernel(uint64_t *__restrict__ dst, const uint64_t *__restr
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride)
         dst[i] = src[i];
+}
+
+// Bulk-async (TMA engine) copy for large peer reads: one thread per CTA keeps
+// STAGES chunk loads (peer HBM -> smem, cp.async.bulk + mbarrier) in flight and
+// drains each landed chunk with a bulk store to local HBM.  No per-byte SM
+// instructions, so ~148 CTAs keep enough NVLink reads outstanding to reach the
+// link peak (probe: 785 GB/s at 1 GiB vs 774 for the SM loop;
+// profiles/r01_nvlink_probe.txt).  dst, src, n and chunk are multiples of 16.
+namespace bulk {
+constexpr int STAGES = 4;
+constexpr uint32_t CHUNK = 32768;
+constexpr int CTAS = kNumSMs;
+
+__device__ __forceinline__ uint32_t saddr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void load_chunk(char *smem, const char *src, uint32_t bytes,
+                                           uint64_t *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(saddr(smem)),
+        "l"(src), "r"(bytes), "r"(saddr(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(32) bulk_copy_kernel(char *__restrict__ dst,
+                                                       const char *__restrict__ src, uint64_t n) {
+    extern __shared__ __align__(128) char ring[];
+    __shared__ __align__(8) uint64_t full[STAGES];
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < STAGES; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&full[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint64_t nchunks = (n + CHUNK - 1) / CHUNK;
+    auto chunk_bytes = [&](uint64_t c) {
+        return (uint32_t)((c + 1) * CHUNK <= n ? CHUNK : n - c * CHUNK);
+    };
+    uint64_t next = blockIdx.x;
+    for (int s = 0; s < STAGES && next < nchunks; ++s, next += gridDim.x)
+        load_chunk(ring + (size_t)s * CHUNK, src + next * CHUNK, chunk_bytes(next), &full[s]);
+    uint32_t phase = 0;
+    int s = 0;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        asm volatile(
+            "{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::
+                "r"(saddr(&full[s])),
+            "r"(phase)
+            : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         dst + c * CHUNK),
+                     "r"(saddr(ring + (size_t)s * CHUNK)), "r"(chunk_bytes(c))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (next < nchunks) {  // refill slot s once its store has read it
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            load_chunk(ring + (size_t)s * CHUNK, src + next * CHUNK, chunk_bytes(next), &full[s]);
+            next += gridDim.x;
+        }
+        if (++s == STAGES) {
+            s = 0;
+            phase ^= 1;
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+}  // namespace bulk
+
+static int launch_bulk_copy(int device, uint64_t dst, uint64_t src, uint64_t n, cudaStream_t s) {
+    static bool configured[64] = {};
+    const int smem = bulk::STAGES * (int)bulk::CHUNK;
+    if (device < 0 || device >= 64) return DIOMP_BAD_REQUEST;
+    if (!configured[device]) {
+        DIOMP_CUDA_TRY(cudaFuncSetAttribute(bulk::bulk_copy_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        configured[device] = true;
+    }
+    const int64_t chunks = ceil_div((int64_t)n, (int64_t)bulk::CHUNK);
+    const int ctas = (int)(chunks < bulk::CTAS ? chunks : bulk::CTAS);
+    bulk::bulk_copy_kernel<<<ctas, 32, smem, s>>>((char *)dst, (const char *)src, n);
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
 }
 
 static int launch_copy(uint64_t dst, uint64_t src, uint64_t n, cudaStream_t s) {
@@ -353,6 +440,56 @@ int diomp_stream_query(void *stream) {
 int diomp_copy(int device, uint64_t dst, uint64_t src, uint64_t nbytes, void *stream) {
     DIOMP_CUDA_TRY(cudaSetDevice(device));
     return launch_copy(dst, src, nbytes, (cudaStream_t)stream);
+}
+
+// Engine choice for one-sided transfers, from the NVLink probe on B200
+// (profiles/r01_nvlink_probe.txt): SM-issued stores to a peer saturate at
+// ~715 GB/s whatever the kernel shape (16/32 B vectors, TMA bulk stores), while
+// the copy engine reaches 717 / 765 / 779 GB/s at 64 MiB / 256 MiB / 1 GiB and
+// is also ahead from 1 MiB; peer reads are fastest through the bulk-async (TMA)
+// kernel from 16 MiB (785 GB/s at 1 GiB) and through the SM loop below that.
+// Small transfers stay on the SM kernel (lowest issue latency).
+// DIOMP_PUT_ENGINE = auto|sm|ce, DIOMP_GET_ENGINE = auto|sm|tma.
+static uint64_t g_put_ce_min = ~0ull, g_get_bulk_min = ~0ull;
+static std::once_flag g_engine_once;
+
+static void init_engines() {
+    std::call_once(g_engine_once, [] {
+        const char *pe = getenv("DIOMP_PUT_ENGINE");
+        const char *ge = getenv("DIOMP_GET_ENGINE");
+        g_put_ce_min = (pe && !strcmp(pe, "sm")) ? ~0ull : (pe && !strcmp(pe, "ce")) ? 1 : (64ull << 10);
+        g_get_bulk_min = (ge && !strcmp(ge, "sm")) ? ~0ull : (ge && !strcmp(ge, "tma")) ? 16 : (16ull << 20);
+    });
+}
+
+int diomp_put(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int remote, void *stream) {
+    if (nbytes == 0) return DIOMP_OK;
+    init_engines();
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    if (remote && nbytes >= g_put_ce_min) {
+        DIOMP_CUDA_TRY(cudaMemcpyAsync((void *)dst, (const void *)src, nbytes,
+                                       cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+        return DIOMP_OK;
+    }
+    return launch_copy(dst, src, nbytes, (cudaStream_t)stream);
+}
+
+int diomp_get(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int remote, void *stream) {
+    if (nbytes == 0) return DIOMP_OK;
+    init_engines();
+    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (remote && nbytes >= g_get_bulk_min && ((dst ^ src) & 15) == 0) {
+        uint64_t head = (16 - (dst & 15)) & 15;
+        uint64_t body = (nbytes - head) / 16 * 16;
+        uint64_t tail = nbytes - head - body;
+        int rc;
+        if (head && (rc = launch_copy(dst, src, head, s))) return rc;
+        if (body && (rc = launch_bulk_copy(device, dst + head, src + head, body, s))) return rc;
+        if (tail && (rc = launch_copy(dst + head + body, src + head + body, tail, s))) return rc;
+        return DIOMP_OK;
+    }
+    return launch_copy(dst, src, nbytes, s);
 }
 
 int diomp_memcpy_async(uint64_t dst, uint64_t src, uint64_t nbytes, int kind, void *stream) {

@@ -144,3 +144,57 @@ def test_device_flag_mode_back_to_back():
         want = O.allreduce_fold([np.random.default_rng(rep * 10 + r).uniform(-1, 1, count)
                                  .astype(np.float32) for r in range(k)], "sum").tobytes()
         assert all(r[rep] == want for r in res)
+
+
+@need_gpus(2)
+@pytest.mark.parametrize("ce_min", [None, 8 * MIB])
+def test_allreduce_device_flag_algorithms_bitwise(ce_min):
+    """Device-flag rings, both allreduce algorithms (fused; fold + copy-engine
+    push from ce_min bytes): bitwise equal to the reference fold order, odd
+    counts, offsets that are not 16-byte aligned, in place and out of place,
+    back to back."""
+    from oracle import oracle as O
+    from paper_2506_02486_b200 import GlobalAddress
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200.emulate import run_emulated
+    k = min(NGPU, 4)
+    cases = [("f32", "sum", (16 * MIB) // 4 + 3, 4), ("f64", "sum", 3 * MIB + 1, 8),
+             ("i32", "max", 4 * MIB + 5, 12), ("f32", "min", 1000, 0), ("i64", "sum", MIB + 7, 0)]
+
+    def contrib(r, et, count, i):
+        rng = np.random.default_rng(900 + 10 * i + r)
+        if et[0] == "f":
+            return rng.uniform(-1, 1, count).astype(DT[et])
+        return rng.integers(-2**30, 2**30, count).astype(DT[et])
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        assert comm.device_sync
+        send = rt.alloc_symmetric(25 * MIB, 0)
+        recv = rt.alloc_symmetric(25 * MIB, 0)
+        outs = []
+        for i, (et, kind, count, delta) in enumerate(cases):
+            op = coll.ReduceOp(coll.ReduceKind(kind), coll.ElementType(et))
+            isz = np.dtype(DT[et]).itemsize
+            s = GlobalAddress(rt.rank, 0, send.addr.offset + delta)
+            for in_place in (False, True):
+                r = s if in_place else GlobalAddress(rt.rank, 0, recv.addr.offset + delta)
+                v = contrib(rt.rank, et, count, i)
+                rt.gm.view(0, s.offset, v.nbytes)[:] = v.tobytes()
+                coll.allreduce(comm, s, r, count, op)
+                outs.append(bytes(rt.gm.view(0, r.offset, count * isz)))
+        return outs
+
+    from paper_2506_02486_b200 import _native
+    if ce_min is not None:
+        _native.call("diomp_set_allreduce_ce_min", ce_min)
+    try:
+        res = run_emulated(k, fn, segment_bytes=256 * MIB)
+    finally:
+        _native.call("diomp_set_allreduce_ce_min", (1 << 64) - 1)
+    j = 0
+    for i, (et, kind, count, delta) in enumerate(cases):
+        want = O.allreduce_fold([contrib(r, et, count, i) for r in range(k)], kind).tobytes()
+        for _ in (False, True):
+            assert all(out[j] == want for out in res), (et, kind, count, delta)
+            j += 1

@@ -5,6 +5,7 @@
 //   tma-store : cp.async.bulk HBM->smem, cp.async.bulk smem->remote (put)
 //   ce        : cudaMemcpyPeerAsync (copy engine)
 // nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o gpurun_out/nvlink_probe tools/nvlink_probe.cu
+#include <chrono>
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
@@ -44,6 +45,27 @@ __global__ void __launch_bounds__(1024) copy16_chunk(uint4 *__restrict__ dst,
         for (int u = 0; u < U; ++u) dst[i + u * blockDim.x] = v[u];
     }
     for (; i < e; i += blockDim.x) dst[i] = src[i];
+}
+
+template <int U, int MODE>
+__global__ void __launch_bounds__(1024) copy32(uint4 *__restrict__ dst, const uint4 *__restrict__ src,
+                                               uint64_t n32) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n32; i += stride) {
+        const char *s = (const char *)src + i * 32;
+        char *d = (char *)dst + i * 32;
+        uint32_t r[8];
+        asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "l"(s));
+        if (MODE == 0)
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(d), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+                         "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]) : "memory");
+        else
+            asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(d), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+                         "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]) : "memory");
+    }
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -130,7 +152,8 @@ struct Args {
     int blocks, threads, kind, u;
     uint32_t chunk;
     int stages;
-    cudaStream_t st;
+    cudaStream_t st, st2;
+    cudaEvent_t ev;
     int srcdev, dstdev;
 };
 
@@ -153,6 +176,20 @@ static void run(void *p) {
         else tma_copy<8><<<a->blocks, 32, smem, a->st>>>(a->dst, a->src, a->n, a->chunk);
         break;
     }
+    case 4:
+        copy32<1, 0><<<a->blocks, a->threads, 0, a->st>>>((uint4 *)a->dst, (uint4 *)a->src, a->n / 32);
+        break;
+    case 5:
+        copy32<1, 1><<<a->blocks, a->threads, 0, a->st>>>((uint4 *)a->dst, (uint4 *)a->src, a->n / 32);
+        break;
+    case 6: {  // CE for 3/4, SM for 1/4 on a second stream
+        uint64_t h = a->n / 4 * 3 / 16 * 16;
+        CK(cudaMemcpyPeerAsync(a->dst, a->dstdev, a->src, a->srcdev, h, a->st));
+        copy16<4><<<a->blocks, a->threads, 0, a->st2>>>((uint4 *)(a->dst + h), (uint4 *)(a->src + h), (a->n - h) / 16);
+        cudaEventRecord(a->ev, a->st2);
+        cudaStreamWaitEvent(a->st, a->ev, 0);
+        break;
+    }
     case 3:
         CK(cudaMemcpyPeerAsync(a->dst, a->dstdev, a->src, a->srcdev, a->n, a->st));
         break;
@@ -165,7 +202,8 @@ int main(int argc, char **argv) {
     if (ndev < 2) { printf("need 2 GPUs\n"); return 1; }
     const uint64_t maxn = 1ull << 30;
     char *buf[2][2];
-    cudaStream_t st[2];
+    cudaStream_t st[2], st2[2];
+    cudaEvent_t ev[2];
     for (int d = 0; d < 2; ++d) {
         CK(cudaSetDevice(d));
         CK(cudaDeviceEnablePeerAccess(1 - d, 0));
@@ -173,6 +211,8 @@ int main(int argc, char **argv) {
         CK(cudaMalloc(&buf[d][1], maxn));
         CK(cudaMemset(buf[d][0], d + 1, maxn));
         CK(cudaStreamCreateWithFlags(&st[d], cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&st2[d], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev[d], cudaEventDisableTiming));
         CK(cudaFuncSetAttribute(tma_copy<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CK(cudaFuncSetAttribute(tma_copy<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     }
@@ -180,24 +220,9 @@ int main(int argc, char **argv) {
     uint64_t sizes[] = {1ull << 20, 8ull << 20, 64ull << 20, 256ull << 20, 1ull << 30};
     struct V { const char *name; int kind, side, blocks, threads, u; uint32_t chunk; int stages; } vs[] = {
         {"put sm 592x512 u4", 0, 0, 592, 512, 4, 0, 0},
-        {"put sm 296x512 u4", 0, 0, 296, 512, 4, 0, 0},
-        {"put sm 148x1024 u4", 0, 0, 148, 1024, 4, 0, 0},
-        {"put sm 1184x256 u4", 0, 0, 1184, 256, 4, 0, 0},
-        {"put sm 592x512 u8", 0, 0, 592, 512, 8, 0, 0},
-        {"put sm 296x512 u2", 0, 0, 296, 512, 2, 0, 0},
-        {"put chunk 592x512 u4", 1, 0, 592, 512, 4, 0, 0},
-        {"put chunk 296x1024 u8", 1, 0, 296, 1024, 8, 0, 0},
-        {"put tma 148 x 4x32K", 2, 0, 148, 32, 0, 32768, 4},
-        {"put tma 296 x 4x16K", 2, 0, 296, 32, 0, 16384, 4},
-        {"put tma 148 x 8x16K", 2, 0, 148, 32, 0, 16384, 8},
-        {"put tma 444 x 4x16K", 2, 0, 444, 32, 0, 16384, 4},
         {"put ce", 3, 0, 0, 0, 0, 0, 0},
         {"get sm 592x512 u4", 0, 1, 592, 512, 4, 0, 0},
-        {"get sm 296x1024 u4", 0, 1, 296, 1024, 4, 0, 0},
-        {"get tma 148 x 8x16K", 2, 1, 148, 32, 0, 16384, 8},
-        {"get ce", 3, 1, 0, 0, 0, 0, 0},
-        {"local sm 592x512 u4", 0, 2, 592, 512, 4, 0, 0},
-        {"local tma 148 x 8x16K", 2, 2, 148, 32, 0, 16384, 8},
+        {"get tma 148 x 4x32K", 2, 1, 148, 32, 0, 32768, 4},
     };
     printf("{\"probe\": \"nvlink\", \"rows\": [\n");
     bool first = true;
@@ -214,7 +239,7 @@ int main(int argc, char **argv) {
             } else {
                 launch = 0; a.src = buf[0][0]; a.dst = buf[0][1]; a.srcdev = 0; a.dstdev = 0;
             }
-            a.st = st[launch];
+            a.st = st[launch]; a.st2 = st2[launch]; a.ev = ev[launch];
             int iters = n >= (256ull << 20) ? 10 : 50;
             float ms = time_it(launch, a.st, iters, run, &a);
             CK(cudaGetLastError());
@@ -225,9 +250,46 @@ int main(int argc, char **argv) {
         }
     }
     printf("\n]}\n");
+    // bidirectional: both GPUs move n bytes toward each other at once (host-timed)
+    struct B { const char *name; int kind, mode, blocks, threads, u; uint32_t chunk; int stages; } bs[] = {
+        {"bidir put sm", 0, 0, 592, 512, 4, 0, 0},
+        {"bidir put ce", 3, 0, 0, 0, 0, 0, 0},
+        {"bidir get sm", 0, 1, 592, 512, 4, 0, 0},
+        {"bidir get tma", 2, 1, 148, 32, 0, 32768, 4},
+        {"bidir get ce", 3, 1, 0, 0, 0, 0, 0},
+        {"bidir put ce + get tma", 9, 2, 148, 32, 0, 32768, 4},
+    };
+    uint64_t bsz[] = {64ull << 20, 256ull << 20, 1ull << 30};
+    for (auto &b : bs) {
+        for (uint64_t n : bsz) {
+            Args a[2];
+            for (int g = 0; g < 2; ++g) {
+                Args &x = a[g];
+                x.n = n; x.blocks = b.blocks; x.threads = b.threads; x.u = b.u; x.chunk = b.chunk; x.stages = b.stages;
+                x.kind = b.kind;
+                int o = 1 - g;
+                if (b.mode == 0 || (b.mode == 2 && g == 0)) {  // put from g to o
+                    if (b.mode == 2) x.kind = 3;
+                    x.src = buf[g][0]; x.dst = buf[o][1]; x.srcdev = g; x.dstdev = o;
+                } else {  // get on g from o
+                    if (b.mode == 2) x.kind = 2;
+                    x.src = buf[o][0]; x.dst = buf[g][1]; x.srcdev = o; x.dstdev = g;
+                }
+                x.st = st[g]; x.st2 = st2[g]; x.ev = ev[g];
+            }
+            int iters = n >= (256ull << 20) ? 10 : 40;
+            for (int w = 0; w < 2; ++w) for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); run(&a[g]); }
+            for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); CK(cudaStreamSynchronize(st[g])); }
+            auto t0 = std::chrono::steady_clock::now();
+            for (int i = 0; i < iters; ++i) for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); run(&a[g]); }
+            for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); CK(cudaStreamSynchronize(st[g])); }
+            double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / iters;
+            printf("BIDIR %-26s %6llu MiB  %.1f GB/s per direction\n", b.name, (unsigned long long)(n >> 20), n / sec / 1e9);
+        }
+    }
     // verify last put byte pattern once
     CK(cudaSetDevice(0));
-    Args a{buf[1][1], buf[0][0], 1ull << 20, 592, 512, 0, 4, 0, 0, st[0], 0, 1};
+    Args a{buf[1][1], buf[0][0], 1ull << 20, 592, 512, 0, 4, 0, 0, st[0], st2[0], ev[0], 0, 1};
     CK(cudaMemset(buf[1][1], 0, 1 << 20));
     CK(cudaDeviceSynchronize());
     a.kind = 2; a.blocks = 148; a.chunk = 16384; a.stages = 8;
