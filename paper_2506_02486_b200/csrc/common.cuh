@@ -78,12 +78,18 @@ __device__ __forceinline__ bool wait_ge(const uint64_t *flag, uint64_t value) {
 
 // "Last CTA out" detection: every CTA calls this once at the very end (after
 // its own global / peer stores); exactly one CTA gets true, after all others
-// have made their stores visible at system scope.  The counter self-resets.
-__device__ __forceinline__ bool last_cta_done(unsigned int *counter, unsigned int nctas) {
+// have made their stores visible.  CTAs that stored to peer memory pass
+// sys_fence (system-scope fence); CTAs that only touched their own GPU's
+// memory need just a GPU-scope fence -- the winner's system fence and release
+// store make the whole grid's work visible to the peers (cumulativity) -- and
+// skip the costly system fence.  The counter self-resets.
+__device__ __forceinline__ bool last_cta_done(unsigned int *counter, unsigned int nctas,
+                                              bool sys_fence = true) {
     __shared__ unsigned int s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
+        if (sys_fence) __threadfence_system();
+        else __threadfence();
         unsigned int prev = atomicAdd(counter, 1u);
         s_last = (prev == nctas - 1);
         if (s_last) {

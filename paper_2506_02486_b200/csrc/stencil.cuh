@@ -34,7 +34,10 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <map>
 #include <mutex>
+#include <queue>
+#include <vector>
 
 #include "common.cuh"
 
@@ -91,6 +94,7 @@ struct Params {
     uint64_t *sig_r;
     uint64_t sl, sr;
     unsigned int *counter;
+    int32_t edge_first;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -293,10 +297,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t *pempty = pfull + NPREV;
 
     // Unit decode: interior chunks first, the two edge chunks (which wait on
-    // and write to the neighbours) last.
+    // and write to the neighbours) last -- or, with edge_first, the edge
+    // chunks first so their NVLink halo stores drain under the interior.
     int c = blockIdx.x / p.ncols;
     const int col = blockIdx.x % p.ncols;
-    if (p.nch > 2) c = (c < p.nch - 2) ? c + 1 : (c == p.nch - 2 ? 0 : p.nch - 1);
+    if (p.nch > 2 && !p.edge_first) c = (c < p.nch - 2) ? c + 1 : (c == p.nch - 2 ? 0 : p.nch - 1);
+    if (p.nch > 2 && p.edge_first) c = (c == 0) ? 0 : (c == 1 ? p.nch - 1 : c - 1);
     const int ty = col / p.ntz, tz = col % p.ntz;
     const int y0 = R + ty * TY, z0 = R + tz * TZ;
     const int64_t xa = R + (int64_t)c * p.chunk;
@@ -371,7 +377,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         else consume<false>(p, sm, full, empty, psm, pfull, pempty, ln, L);
     }
 
-    if (p.sync && last_cta_done(p.counter, gridDim.x) && threadIdx.x == 0) {
+    const bool wrote_peer = (xa < 2 * R && p.left_next) || (xb > p.NX - 2 * R && p.right_next);
+    if (p.sync && last_cta_done(p.counter, gridDim.x, wrote_peer) && threadIdx.x == 0) {
         if (p.sig_l) st_release_sys(p.sig_l, p.sl);
         if (p.sig_r) st_release_sys(p.sig_r, p.sr);
     }
@@ -456,10 +463,37 @@ static bool fast_path_ok(uint64_t u_next, uint64_t u_cur, uint64_t u_prev, int64
     return true;
 }
 
-// Chunking along x: pick the chunk count minimising
-// rounds(units over resident CTA slots) x (chunk + warm-up cost).
+// Chunking along x.  Units (column, chunk) are handed to SMs in blockIdx
+// order as CTAs retire, so the step time is the makespan of that list
+// schedule on kNumSMs slots with unit cost (planes + W); W = 4 planes of
+// warm-up (the 2R extra u_cur planes and the pipeline fill) was fitted to
+// chunk sweeps at 128 and 256 planes on B200 (tools/probe.py stencil 1024 NX
+// with DIOMP_STENCIL_CHUNK).  Simulate each chunk count, keep the best;
+// results are cached per shape.
+static double list_makespan(int64_t nx_int, int ncols, int64_t chunk) {
+    constexpr double W = 4.0;
+    const int64_t nch = ceil_div(nx_int, chunk);
+    std::priority_queue<double, std::vector<double>, std::greater<double>> slot;
+    for (int i = 0; i < kNumSMs; ++i) slot.push(0.0);
+    for (int64_t b = 0; b < nch; ++b) {
+        int64_t c = b;  // interior chunks first, then the two edge chunks
+        if (nch > 2) c = (b < nch - 2) ? b + 1 : (b == nch - 2 ? 0 : nch - 1);
+        const double len = (double)(c == nch - 1 ? nx_int - c * chunk : chunk) + W;
+        for (int u = 0; u < ncols; ++u) {
+            const double t = slot.top();
+            slot.pop();
+            slot.push(t + len);
+        }
+    }
+    double t = 0;
+    while (!slot.empty()) {
+        t = slot.top();
+        slot.pop();
+    }
+    return t;
+}
+
 static void pick_chunks(int64_t nx_int, int ncols, int *chunk_out, int *nch_out) {
-    const int slots = kNumSMs;  // one CTA per SM
     const char *env = getenv("DIOMP_STENCIL_CHUNK");
     if (env && atoi(env) > 0) {
         int ch = atoi(env);
@@ -468,20 +502,34 @@ static void pick_chunks(int64_t nx_int, int ncols, int *chunk_out, int *nch_out)
         *nch_out = (int)ceil_div(nx_int, ch);
         return;
     }
-    double best = 1e300;
-    int best_nch = 1;
-    for (int nch = 1; nch <= 64; ++nch) {
-        int64_t chunk = ceil_div(nx_int, nch);
-        if (nch > 1 && chunk < 2 * R) break;
-        int64_t units = (int64_t)ncols * ceil_div(nx_int, chunk);
-        double rounds = (double)ceil_div(units, slots);
-        double cost = rounds * ((double)chunk + 0.35 * 2 * R);
-        if (cost < best * 0.999) {
-            best = cost;
-            best_nch = nch;
+    static std::mutex mu;
+    static std::map<std::pair<int64_t, int>, int64_t> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(nx_int, ncols);
+    auto it = cache.find(key);
+    int64_t chunk;
+    if (it != cache.end()) {
+        chunk = it->second;
+    } else {
+        double best = 1e300;
+        chunk = nx_int;
+        // chunk counts 1..16, and uneven splits (a long chunk plus a short
+        // tail) between consecutive counts
+        for (int nch = 1; nch <= 16; ++nch) {
+            const int64_t hi = ceil_div(nx_int, nch), lo = ceil_div(nx_int, nch + 1);
+            if (nch > 1 && hi < 2 * R) break;
+            for (int j = 0; j < 8; ++j) {
+                const int64_t ch = hi - (hi - lo) * j / 8;
+                if (ch < 2 * R || (j && ch == hi)) continue;
+                const double t = list_makespan(nx_int, ncols, ch);
+                if (t < best * 0.999) {
+                    best = t;
+                    chunk = ch;
+                }
+            }
         }
+        cache[key] = chunk;
     }
-    int64_t chunk = ceil_div(nx_int, best_nch);
     *chunk_out = (int)chunk;
     *nch_out = (int)ceil_div(nx_int, chunk);
 }
@@ -575,6 +623,7 @@ int diomp_stencil_run(const diomp_stencil_plan *pl, int64_t step0, int64_t nstep
                    make_plane_map(&pmaps[b], (const double *)pl->field[b], pl->NX, pl->NY, pl->NZ, false) == DIOMP_OK;
     }
     const int64_t plane = pl->NY * pl->NZ;
+    static const int edge_first = getenv("DIOMP_STENCIL_EDGE_FIRST") ? atoi(getenv("DIOMP_STENCIL_EDGE_FIRST")) : 0;
     for (int64_t st = step0; st < step0 + nsteps; ++st) {
         const int pb = (int)(st & 1), cb = 1 - pb;  // prev = field[s%2], cur = field[(s+1)%2]
         const int64_t k = st - step0;
@@ -591,6 +640,7 @@ int diomp_stencil_run(const diomp_stencil_plan *pl, int64_t step0, int64_t nstep
             p.src_x = pl->src_i; p.src_y = pl->src_j; p.src_z = pl->src_k;
             p.amp = pl->amp;
             p.sync = pl->sync;
+            p.edge_first = edge_first;
             if (pl->sync) {
                 p.wait_l = pl->left_field[pb] ? (const uint64_t *)pl->wait_left : nullptr;
                 p.wait_r = pl->right_field[pb] ? (const uint64_t *)pl->wait_right : nullptr;

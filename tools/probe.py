@@ -2,7 +2,7 @@
 
     python tools/probe.py dgemm [N]      DMMA DGEMM vs cuBLAS (torch.matmul f64)
     python tools/probe.py copy           SM copy kernel (local D2D), 8 B .. 1 GiB
-    python tools/probe.py stencil [G]    stencil_update seam on a G^3 field
+    python tools/probe.py stencil [G [NX]] stencil_update seam on a G^3 field / NX x G x G slab
 """
 
 from __future__ import annotations
@@ -59,18 +59,22 @@ def copy():
     return {"probe": "copy_local", "rows": out}
 
 
-def stencil(g=512):
+def stencil(g=512, nx=None):
+    """stencil_update seam on a g^3 grid, or an nx x g x g slab (the per-GPU
+    share of a g^3 grid over g/nx GPUs, without the halo exchange)."""
     import torch
 
     from paper_2506_02486_b200 import kernels
     from paper_2506_02486_b200.apps.stencil import _time_params
     _, w = _time_params(4)
-    shape = (g + 8, g + 8, g + 8)
+    nx = g if nx is None else nx
+    shape = (nx + 8, g + 8, g + 8)
     a = torch.rand(shape, dtype=torch.float64, device="cuda")
     b = torch.rand(shape, dtype=torch.float64, device="cuda")
     ms = _time(lambda: kernels.stencil_update(b, a, b, 3 * w[0], w, w, w, 4), iters=10)
-    return {"probe": "stencil_update", "grid": g, "ms": ms, "gpts": g ** 3 / ms / 1e6,
-            "GBps_24B": 24 * g ** 3 / ms / 1e6}
+    pts = nx * g * g
+    return {"probe": "stencil_update", "grid": [nx, g, g], "ms": ms, "gpts": pts / ms / 1e6,
+            "GBps_24B": 24 * pts / ms / 1e6}
 
 
 def triad(n_gb=8):
