@@ -11,7 +11,8 @@
 //    has no f64 kind, so the FP64 tensor path on Blackwell is DMMA
 //    (mma.sync.m8n8k4.f64; the larger f64 shapes expand to the same DMMA.8x8x4
 //    on sm_100a).  Default tiles 128x64x16, 8 warps of 32x32, 2 CTAs/SM,
-//    3-stage cp.async pipeline into bank-conflict-free padded tiles.  When `fwd` is
+//    3-stage cp.async pipeline into bank-conflict-free padded tiles, A
+//    fragments of two k-steps fetched with one 16 B shared load.  When `fwd` is
 //    set, every B tile is additionally stored once to the predecessor's spare
 //    stripe over NVLink straight from shared memory (CTA row mi forwards the
 //    k-tiles kt with kt % n_mtiles == mi), fusing the ring shift of
@@ -80,13 +81,15 @@ __global__ void __launch_bounds__(256) matmul_exact_kernel(int64_t n, int64_t kk
 // ---------------------------------------------------------------------------
 // Tile configurations.  WM x WN = 8x8 DMMA fragments per warp; WARPS_M x
 // WARPS_N warps per CTA; MINB CTAs per SM (register budget).
-template <int WM_, int WN_, int WARPS_M_, int WARPS_N_, int BK_, int STAGES_, int MINB_>
+template <int WM_, int WN_, int WARPS_M_, int WARPS_N_, int BK_, int STAGES_, int MINB_,
+          bool PAIRK_ = false, int APADX_ = 4>
 struct Cfg {
     static constexpr int WM = WM_, WN = WN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+    static constexpr bool PAIRK = PAIRK_;
     static constexpr int BM = WM * 8 * WARPS_M, BN = WN * 8 * WARPS_N, BK = BK_;
     static constexpr int STAGES = STAGES_, MINB = MINB_;
     static constexpr int THREADS = WARPS_M * WARPS_N * 32;
-    static constexpr int APAD = BK + 4;   // A tile row pitch (doubles): conflict-free fragments
+    static constexpr int APAD = BK + APADX_;  // A tile row pitch (doubles): conflict-free fragments
     static constexpr int BPAD = BN + 4;   // B tile row pitch
     static constexpr int A_STAGE = BM * APAD, B_STAGE = BK * BPAD;
     static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
@@ -94,6 +97,10 @@ struct Cfg {
 using CfgBig = Cfg<8, 4, 2, 4, 16, 4, 1>;    // 128x128 CTA, 64x32 warps, 1 CTA/SM
 using CfgDual = Cfg<4, 4, 4, 2, 16, 3, 2>;   // 128x64 CTA, 32x32 warps, 2 CTAs/SM
 using CfgDeepK = Cfg<8, 4, 2, 4, 32, 3, 1>;  // 128x128 CTA, BK=32 (half the barriers)
+using CfgP1 = Cfg<4, 4, 4, 2, 16, 3, 2, true, 4>;  // CfgDual with paired-k A loads
+using CfgP2 = Cfg<4, 4, 4, 2, 16, 3, 2, true, 8>;  // same, A pitch 24 (conflict-free 16 B rows)
+using CfgP3 = Cfg<8, 4, 2, 4, 16, 4, 1, true, 8>;  // CfgBig with paired-k A loads
+using CfgP4 = Cfg<4, 4, 4, 2, 16, 4, 2, true, 4>;  // paired-k, 4 stages, 2 CTAs/SM
 
 struct GemmParams {
     int64_t M, N, K;
@@ -217,17 +224,45 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_dmma_kernel(const _
                         *reinterpret_cast<const double2 *>(b_s + r * C::BPAD + ch * 2);
             }
         }
+        if (C::PAIRK) {
+            // k pairs: lane tq takes k = kk+2tq (first DMMA) and kk+2tq+1
+            // (second) -- one 16 B shared load gives both A fragments; the
+            // 8-wide k slice is summed in a different (still exact-product,
+            // rounded-add) order, inside the GEMM's stated tolerance.
 #pragma unroll
-        for (int kk = 0; kk < C::BK; kk += 4) {
-            double af[C::WM], bf[C::WN];
+            for (int kk = 0; kk < C::BK; kk += 8) {
+                double2 a2[C::WM];
+                double b0[C::WN], b1[C::WN];
 #pragma unroll
-            for (int i = 0; i < C::WM; ++i) af[i] = a_s[(wm + i * 8 + gq) * C::APAD + kk + tq];
+                for (int i = 0; i < C::WM; ++i)
+                    a2[i] = *reinterpret_cast<const double2 *>(a_s + (wm + i * 8 + gq) * C::APAD + kk + 2 * tq);
 #pragma unroll
-            for (int j = 0; j < C::WN; ++j) bf[j] = b_s[(kk + tq) * C::BPAD + wn + j * 8 + gq];
+                for (int j = 0; j < C::WN; ++j) {
+                    b0[j] = b_s[(kk + 2 * tq) * C::BPAD + wn + j * 8 + gq];
+                    b1[j] = b_s[(kk + 2 * tq + 1) * C::BPAD + wn + j * 8 + gq];
+                }
 #pragma unroll
-            for (int i = 0; i < C::WM; ++i)
+                for (int i = 0; i < C::WM; ++i)
 #pragma unroll
-                for (int j = 0; j < C::WN; ++j) dmma(acc[i][j], af[i], bf[j]);
+                    for (int j = 0; j < C::WN; ++j) dmma(acc[i][j], a2[i].x, b0[j]);
+#pragma unroll
+                for (int i = 0; i < C::WM; ++i)
+#pragma unroll
+                    for (int j = 0; j < C::WN; ++j) dmma(acc[i][j], a2[i].y, b1[j]);
+            }
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < C::BK; kk += 4) {
+                double af[C::WM], bf[C::WN];
+#pragma unroll
+                for (int i = 0; i < C::WM; ++i) af[i] = a_s[(wm + i * 8 + gq) * C::APAD + kk + tq];
+#pragma unroll
+                for (int j = 0; j < C::WN; ++j) bf[j] = b_s[(kk + tq) * C::BPAD + wn + j * 8 + gq];
+#pragma unroll
+                for (int i = 0; i < C::WM; ++i)
+#pragma unroll
+                    for (int j = 0; j < C::WN; ++j) dmma(acc[i][j], af[i], bf[j]);
+            }
         }
     }
     cp_async_wait<0>();
@@ -308,12 +343,19 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
         p.sig_value[i] = x->sig_value[i];
     }
     p.counter = (unsigned int *)x->counter;
-    // default: 2 CTAs/SM with 32x32 warp tiles (0.91 of cuBLAS DGEMM at 8192^3;
-    // the 1-CTA 64x32 and BK=32 variants measured 0.87 / 0.89)
+    // default: 2 CTAs/SM with 32x32 warp tiles and paired-k A fragments
+    // (16 B shared loads, pitch 24): 0.92 of cuBLAS DGEMM at 8192^3, DMMA pipe
+    // 88 % active vs cuBLAS 96.5 % (profiles/r01_dgemm_dmma_pipe.json).  The
+    // single-k layout measured 0.91, the 1-CTA 64x32 variants 0.86-0.87,
+    // BK=32 0.89, 4 stages at 1 CTA/SM 0.74.
     const char *v = getenv("DIOMP_DGEMM_CFG");
     if (v && atoi(v) == 0) return launch_dgemm<CfgBig>(p, x->device, (cudaStream_t)stream);
+    if (v && atoi(v) == 1) return launch_dgemm<CfgDual>(p, x->device, (cudaStream_t)stream);
     if (v && atoi(v) == 2) return launch_dgemm<CfgDeepK>(p, x->device, (cudaStream_t)stream);
-    return launch_dgemm<CfgDual>(p, x->device, (cudaStream_t)stream);
+    if (v && atoi(v) == 11) return launch_dgemm<CfgP1>(p, x->device, (cudaStream_t)stream);
+    if (v && atoi(v) == 13) return launch_dgemm<CfgP3>(p, x->device, (cudaStream_t)stream);
+    if (v && atoi(v) == 14) return launch_dgemm<CfgP4>(p, x->device, (cudaStream_t)stream);
+    return launch_dgemm<CfgP2>(p, x->device, (cudaStream_t)stream);
 }
 
 }  // extern "C"
