@@ -97,10 +97,8 @@ struct Cfg {
 using CfgBig = Cfg<8, 4, 2, 4, 16, 4, 1>;    // 128x128 CTA, 64x32 warps, 1 CTA/SM
 using CfgDual = Cfg<4, 4, 4, 2, 16, 3, 2>;   // 128x64 CTA, 32x32 warps, 2 CTAs/SM
 using CfgDeepK = Cfg<8, 4, 2, 4, 32, 3, 1>;  // 128x128 CTA, BK=32 (half the barriers)
-using CfgP1 = Cfg<4, 4, 4, 2, 16, 3, 2, true, 4>;  // CfgDual with paired-k A loads
-using CfgP2 = Cfg<4, 4, 4, 2, 16, 3, 2, true, 8>;  // same, A pitch 24 (conflict-free 16 B rows)
-using CfgP3 = Cfg<8, 4, 2, 4, 16, 4, 1, true, 8>;  // CfgBig with paired-k A loads
-using CfgP4 = Cfg<4, 4, 4, 2, 16, 4, 2, true, 4>;  // paired-k, 4 stages, 2 CTAs/SM
+using CfgP2 = Cfg<4, 4, 4, 2, 16, 3, 2, true, 8>;  // CfgDual, paired-k A loads, A pitch 24
+using CfgQ4 = Cfg<4, 8, 2, 2, 16, 3, 2, false, 4>; // 64x128 CTA, 4 warps of 32x64 (cuBLAS's shape)
 
 struct GemmParams {
     int64_t M, N, K;
@@ -346,15 +344,14 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
     // default: 2 CTAs/SM with 32x32 warp tiles and paired-k A fragments
     // (16 B shared loads, pitch 24): 0.92 of cuBLAS DGEMM at 8192^3, DMMA pipe
     // 88 % active vs cuBLAS 96.5 % (profiles/r01_dgemm_dmma_pipe.json).  The
-    // single-k layout measured 0.91, the 1-CTA 64x32 variants 0.86-0.87,
-    // BK=32 0.89, 4 stages at 1 CTA/SM 0.74.
+    // single-k layout measured 0.91, cuBLAS's own 64x128 / 32x64-warp shape
+    // 0.91-0.93, the 1-CTA 64x32 variants 0.86-0.87, BK=32 0.89, 4 stages at
+    // 1 CTA/SM 0.74.
     const char *v = getenv("DIOMP_DGEMM_CFG");
     if (v && atoi(v) == 0) return launch_dgemm<CfgBig>(p, x->device, (cudaStream_t)stream);
     if (v && atoi(v) == 1) return launch_dgemm<CfgDual>(p, x->device, (cudaStream_t)stream);
     if (v && atoi(v) == 2) return launch_dgemm<CfgDeepK>(p, x->device, (cudaStream_t)stream);
-    if (v && atoi(v) == 11) return launch_dgemm<CfgP1>(p, x->device, (cudaStream_t)stream);
-    if (v && atoi(v) == 13) return launch_dgemm<CfgP3>(p, x->device, (cudaStream_t)stream);
-    if (v && atoi(v) == 14) return launch_dgemm<CfgP4>(p, x->device, (cudaStream_t)stream);
+    if (v && atoi(v) == 3) return launch_dgemm<CfgQ4>(p, x->device, (cudaStream_t)stream);
     return launch_dgemm<CfgP2>(p, x->device, (cudaStream_t)stream);
 }
 
