@@ -148,34 +148,49 @@ __device__ __forceinline__ void fold_range(const Args &a, uint64_t lo, uint64_t 
     auto vsrc = [&](int p) { return reinterpret_cast<const VT *>(src(p) + vlo); };
     auto vdst = [&](int p) { return reinterpret_cast<VT *>(dst(p) + vlo); };
     const uint64_t nvec = (vhi - vlo) / V;
-    for (uint64_t v = gtid; v < nvec; v += gsz) {
-        VT buf[KMAX];
+    // U independent vectors per thread per iteration: all k*U loads are in
+    // flight before the first fold (NVLink load latency ~2 us needs MBs in
+    // flight per GPU)
+    constexpr int U = KMAX <= 4 ? 2 : 1;
+    for (uint64_t v0 = gtid; v0 < nvec; v0 += gsz * U) {
+        VT buf[U][KMAX];
 #pragma unroll
-        for (int i = 0; i < KMAX; ++i)
-            if (i < k) {
-                int pidx = start + i;
-                if (pidx >= k) pidx -= k;
-                buf[i] = vsrc(pidx)[v];
+        for (int u = 0; u < U; ++u) {
+            const uint64_t v = v0 + u * gsz;
+            if (v < nvec) {
+#pragma unroll
+                for (int i = 0; i < KMAX; ++i)
+                    if (i < k) {
+                        int pidx = start + i;
+                        if (pidx >= k) pidx -= k;
+                        buf[u][i] = vsrc(pidx)[v];
+                    }
             }
-        T acc[V];
-        const T *b0 = reinterpret_cast<const T *>(&buf[0]);
+        }
 #pragma unroll
-        for (int e = 0; e < V; ++e) acc[e] = b0[e];
+        for (int u = 0; u < U; ++u) {
+            const uint64_t v = v0 + u * gsz;
+            if (v >= nvec) break;
+            T acc[V];
+            const T *b0 = reinterpret_cast<const T *>(&buf[u][0]);
 #pragma unroll
-        for (int i = 1; i < KMAX; ++i)
-            if (i < k) {
-                const T *bi = reinterpret_cast<const T *>(&buf[i]);
+            for (int e = 0; e < V; ++e) acc[e] = b0[e];
 #pragma unroll
-                for (int e = 0; e < V; ++e) acc[e] = OP::apply(acc[e], bi[e]);
-            }
-        VT out = *reinterpret_cast<VT *>(acc);
-        if (only >= 0) {
-            vdst(only)[v] = out;
-        } else {
-            for (int i = 0; i < k; ++i) {
-                int pidx = t.pos + i;  // own copy first, then peers
-                if (pidx >= k) pidx -= k;
-                vdst(pidx)[v] = out;
+            for (int i = 1; i < KMAX; ++i)
+                if (i < k) {
+                    const T *bi = reinterpret_cast<const T *>(&buf[u][i]);
+#pragma unroll
+                    for (int e = 0; e < V; ++e) acc[e] = OP::apply(acc[e], bi[e]);
+                }
+            VT out = *reinterpret_cast<VT *>(acc);
+            if (only >= 0) {
+                vdst(only)[v] = out;
+            } else {
+                for (int i = 0; i < k; ++i) {
+                    int pidx = t.pos + i;  // own copy first, then peers
+                    if (pidx >= k) pidx -= k;
+                    vdst(pidx)[v] = out;
+                }
             }
         }
     }
@@ -306,7 +321,11 @@ static int launch_reduce(Args a, cudaStream_t s) {
     const int g = grid_for(items);
     const bool ce = a.mode == 0 && a.t.sync && a.t.k > 1 && a.count * sizeof(T) >= ar_ce_min();
     if (ce) a.mode = 2;
-    if (a.t.k <= 8) reduce_kernel<T, OP, 8><<<g, THREADS, 0, s>>>(a);
+    // KMAX = smallest supported team bound >= k (register footprint, and the
+    // per-thread unroll, follow the actual team size)
+    if (a.t.k <= 2) reduce_kernel<T, OP, 2><<<g, THREADS, 0, s>>>(a);
+    else if (a.t.k <= 4) reduce_kernel<T, OP, 4><<<g, THREADS, 0, s>>>(a);
+    else if (a.t.k <= 8) reduce_kernel<T, OP, 8><<<g, THREADS, 0, s>>>(a);
     else if (a.t.k <= 16) reduce_kernel<T, OP, 16><<<g, THREADS, 0, s>>>(a);
     else reduce_kernel<T, OP, DIOMP_MAX_TEAM><<<g, THREADS, 0, s>>>(a);
     DIOMP_LAUNCH_CHECK();
