@@ -168,6 +168,36 @@ int diomp_set_allreduce_ce_min(uint64_t bytes);
 int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off,
                     uint64_t count, int32_t dtype, int32_t op, void *stream);
 
+/* ---- NVSwitch multicast (NVLS) allreduce: collectives.allreduce
+ *      (collectives.py:326-405) with the reduction done in the switch
+ *      (multimem.ld_reduce) and the result fanned out by one multimem.st.
+ *      Float sums agree with the reference fold within rounding (not
+ *      bitwise); integer sum/min/max are exact; float min/max are refused.
+ *      Setup (collective over the communicator): position 0 creates the
+ *      multicast object and exports it as a POSIX fd (passed to the other
+ *      processes over a Unix socket), every member imports it, adds its GPU,
+ *      then (after a barrier) binds a window of its own HBM.                  */
+int diomp_mc_supported(int device, int *out);
+int diomp_mc_window_bytes(int nmembers, uint64_t want, uint64_t *total_out);
+int diomp_mc_create(int nmembers, uint64_t total, int *fd_out, uint64_t *mc_out);
+int diomp_mc_import(int fd, uint64_t *mc_out);
+int diomp_mc_add_device(uint64_t mc, int device);
+int diomp_mc_bind(uint64_t mc, int device, uint64_t total, uint64_t *uc_out, uint64_t *mc_va_out,
+                  uint64_t *phys_out);
+int diomp_mc_release(uint64_t mc, int device, uint64_t total, uint64_t uc, uint64_t mc_va,
+                     uint64_t phys);
+typedef struct {
+    int32_t device, k, pos, dtype, op, _pad;
+    uint64_t uc, mc;      /* window: own unicast VA / multicast VA (2 MiB flag header first) */
+    uint64_t window;      /* data bytes per round (window size minus the header) */
+    uint64_t send, recv;  /* own device pointers, 16 B aligned; recv may equal send */
+    uint64_t count;       /* elements */
+    uint64_t epoch;       /* rounds completed on this window so far (all members equal) */
+    uint64_t counter;     /* u32 last-CTA counter in own memory */
+} diomp_nvls_args;
+int diomp_allreduce_nvls(const diomp_nvls_args *args, void *stream);
+int diomp_nvls_rounds(uint64_t count, int dtype, uint64_t window, uint64_t *rounds_out);
+
 /* ---- Minimod stencil: kernels/__init__.py:30 seam `stencil_update`
  *      (reference.py:14-31 / _core.pyx:9-32).  One interior update of
  *      (NX, NY, NZ) C-order f64 arrays, ghost width `radius` (<= 8); u_next may

@@ -28,6 +28,13 @@ class Team(ctypes.Structure):
                 ("epoch_to", c_u64 * MAX_TEAM), ("epoch_from", c_u64 * MAX_TEAM)]
 
 
+class NvlsArgs(ctypes.Structure):
+    _fields_ = [("device", c_i32), ("k", c_i32), ("pos", c_i32), ("dtype", c_i32),
+                ("op", c_i32), ("_pad", c_i32), ("uc", c_u64), ("mc", c_u64),
+                ("window", c_u64), ("send", c_u64), ("recv", c_u64), ("count", c_u64),
+                ("epoch", c_u64), ("counter", c_u64)]
+
+
 class StencilArgs(ctypes.Structure):
     _fields_ = [("u_next", c_u64), ("u_cur", c_u64), ("u_prev", c_u64),
                 ("NX", c_i64), ("NY", c_i64), ("NZ", c_i64),
@@ -103,6 +110,16 @@ _PROTOS = {
     "diomp_bcast": [ctypes.POINTER(Team), c_u64, c_u64, c_i32, c_vp],
     "diomp_reduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_i32, c_vp],
     "diomp_set_allreduce_ce_min": [c_u64],
+    "diomp_mc_supported": [ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
+    "diomp_mc_window_bytes": [ctypes.c_int, c_u64, ctypes.POINTER(c_u64)],
+    "diomp_mc_create": [ctypes.c_int, c_u64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(c_u64)],
+    "diomp_mc_import": [ctypes.c_int, ctypes.POINTER(c_u64)],
+    "diomp_mc_add_device": [c_u64, ctypes.c_int],
+    "diomp_mc_bind": [c_u64, ctypes.c_int, c_u64, ctypes.POINTER(c_u64), ctypes.POINTER(c_u64),
+                      ctypes.POINTER(c_u64)],
+    "diomp_mc_release": [c_u64, ctypes.c_int, c_u64, c_u64, c_u64, c_u64],
+    "diomp_allreduce_nvls": [ctypes.POINTER(NvlsArgs), c_vp],
+    "diomp_nvls_rounds": [c_u64, ctypes.c_int, c_u64, ctypes.POINTER(c_u64)],
     "diomp_allreduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_vp],
     "diomp_stencil_update": [ctypes.c_int, ctypes.POINTER(StencilArgs), c_vp],
     "diomp_stencil_run": [ctypes.POINTER(StencilPlan), c_i64, c_i64, c_vp],

@@ -301,19 +301,46 @@ def _coll_cli(args, kind):
         raise UsageError(f"--workload {kind} needs >= 2 GPUs")
     sizes = tuple(1024 << (2 * i) for i in range(11))  # 1 KiB .. 1 GiB (x4)
     bk = BenchKind.Allreduce if kind == "allreduce" else BenchKind.Bcast
-    rows = run_collective(rt, BenchSpec(bk, sizes, iters=max(args.steps, 3),
-                                        warmup=args.warmup))
+    spec = BenchSpec(bk, sizes, iters=max(args.steps, 3), warmup=args.warmup)
+    rows = run_collective(rt, spec)
+    # the in-switch (NVLS) allreduce, where every GPU supports multicast:
+    # float sums within rounding of the exact fold (collectives.allreduce)
+    nvls_rows = None
+    if kind == "allreduce" and os.environ.get("BENCH_NVLS", "1") != "0":
+        from .. import nvls
+        ok = rt.ctrl.allgather(tuple(range(rt.nranks)), "bench/nvls",
+                               bytes([nvls.supported(rt.gpus[0])]))
+        if all(b == b"\x01" for _, b in ok):
+            prev = os.environ.get("DIOMP_ALLREDUCE_ALGO")
+            os.environ["DIOMP_ALLREDUCE_ALGO"] = "nvls"
+            try:
+                nvls_rows = run_collective(rt, spec)
+            finally:
+                if prev is None:
+                    os.environ.pop("DIOMP_ALLREDUCE_ALGO", None)
+                else:
+                    os.environ["DIOMP_ALLREDUCE_ALGO"] = prev
     if rt.rank == 0:
         k = rt.nranks
         factor = 2 * (k - 1) / k if kind == "allreduce" else 1.0
-        table = [(r.size_bytes, round(r.mean_us, 2),
-                  round(factor * r.size_bytes / r.mean_us / 1e3, 2)) for r in rows]
+
+        def tab(rs):
+            return [(r.size_bytes, round(r.mean_us, 2),
+                     round(factor * r.size_bytes / r.mean_us / 1e3, 2)) for r in rs]
+        table = tab(rows)
         value = table[-1][2]
+        extra = {"roofline": {"bound": "nvlink", "achieved": value, "peak": NVLINK_PEER_GBS,
+                              "unit": "GB/s", "frac": round(value / NVLINK_PEER_GBS, 4)},
+                 "rows": table, "row_format": "[bytes, mean_us, busBW GB/s]",
+                 "algorithm": "exact (reference ring-fold order, bitwise)" if kind == "allreduce"
+                 else "p2p"}
+        if nvls_rows:
+            nt = tab(nvls_rows)
+            extra["nvls"] = {"busbw_1GiB": nt[-1][2], "rows": nt,
+                             "algorithm": "NVSwitch multimem.ld_reduce + multimem.st "
+                                          "(f32 sums within rounding of the exact fold)"}
         _line(rt, f"{kind}_busbw_1GiB", value, "GB/s", args,
-              {"workload": f"{kind}_f32_sum_sweep_1KiB_1GiB", "endpoints": k},
-              {"roofline": {"bound": "nvlink", "achieved": value, "peak": NVLINK_PEER_GBS,
-                            "unit": "GB/s", "frac": round(value / NVLINK_PEER_GBS, 4)},
-               "rows": table, "row_format": "[bytes, mean_us, busBW GB/s]"})
+              {"workload": f"{kind}_f32_sum_sweep_1KiB_1GiB", "endpoints": k}, extra)
     rt.finalize()
     return 0
 

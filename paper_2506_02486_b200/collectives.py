@@ -27,7 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from .errors import InvalidAddress, RootOutOfRange, StaleGroup, TypeMismatch
+from .errors import InvalidAddress, RootOutOfRange, StaleGroup, TypeMismatch, UsageError
 from .global_memory import GlobalAddress
 from .runtime import COUNTER_COLL, COUNTER_OFF, Group, Runtime
 from .topology import Endpoint
@@ -261,8 +261,13 @@ def reduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, count: 
 
 
 def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, count: int,
-              op: ReduceOp, *, blocking: bool = True):
-    """Reduce-scatter in ring-fold order + all-gather; in place works."""
+              op: ReduceOp, *, blocking: bool = True, algorithm: str | None = None):
+    """Reduce-scatter in ring-fold order + all-gather; in place works.
+
+    algorithm "exact" (default; DIOMP_ALLREDUCE_ALGO overrides): the
+    reference's fold order, bit-identical.  "nvls": the NVSwitch reduces
+    (multimem.ld_reduce) -- integer results identical, float sums within
+    rounding (rel-L2 1e-6 f32 / 1e-12 f64), float min/max refused."""
     rt, k = comm.rt, comm.size
     _check_typed(send, count, op.etype)
     _check_typed(recv, count, op.etype)
@@ -273,6 +278,9 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
             rt.gm.check_rma_range(ep.device, recv.offset, max(nbytes, 1))
     if count == 0:
         return
+    algo = algorithm or os.environ.get("DIOMP_ALLREDUCE_ALGO", "exact")
+    if algo not in ("exact", "nvls"):
+        raise UsageError(f"unknown allreduce algorithm {algo!r}")
     if k == 1:
         ep = comm.ring[0]
         if send.offset != recv.offset:
@@ -284,9 +292,36 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
             s.synchronize()
         return
     comm._next_seq()
+    if algo == "nvls":
+        _allreduce_nvls(comm, send, recv, count, op, blocking)
+        return
     _run(comm, lambda t, s: _native.lib.diomp_allreduce(t, send.offset, recv.offset, count,
                                                         op.etype.code, op.code, s), blocking,
          signals=3)
+
+
+def _allreduce_nvls(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, count: int,
+                    op: ReduceOp, blocking: bool):
+    from .nvls import NvlsWindow
+    rt = comm.rt
+    if op.etype in (ElementType.f32, ElementType.f64) and op.kind is not ReduceKind.Sum:
+        raise TypeMismatch("nvls allreduce: the switch's float min/max NaN rules are not "
+                           "numpy's; use algorithm='exact'")
+    if send.offset % 16 or recv.offset % 16:
+        raise UsageError("nvls allreduce needs 16-byte aligned send/recv offsets")
+    w = comm.__dict__.get("_nvls")
+    if w is None:
+        w = comm._nvls = NvlsWindow(comm)
+    ep = comm.ring[w.pos]
+    if blocking:
+        _after_torch(rt, ep.device)
+    base = rt.gm.base(ep.device)
+    s = rt._rma_streams[ep.device]
+    w.launch(base + send.offset, base + recv.offset, count, op.etype.code, op.code,
+             rt.counter_address(ep.device, COUNTER_COLL), s.handle)
+    if blocking:
+        s.synchronize()
+        _native.check_device(s.gpu, "allreduce_nvls")
 
 
 def device_bcast(rt: Runtime, var: GlobalAddress, nbytes: int, group: Group):

@@ -9,3 +9,4 @@
 #include "stencil.cuh"
 #include "collectives.cuh"
 #include "gemm.cuh"
+#include "nvls.cuh"

@@ -198,3 +198,67 @@ def test_allreduce_device_flag_algorithms_bitwise(ce_min):
         for _ in (False, True):
             assert all(out[j] == want for out in res), (et, kind, count, delta)
             j += 1
+
+
+@need_gpus(2)
+def test_allreduce_nvls_in_switch(monkeypatch):
+    """NVSwitch multicast allreduce (algorithm="nvls"): integer sum/min/max
+    bitwise equal to the reference fold, float sums within the north-star
+    tolerance (rel-L2 1e-6 f32, 1e-12 f64); several rounds through a small
+    window, in place, back to back with the exact algorithm; float min/max
+    refused."""
+    from oracle import oracle as O
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200 import nvls
+    from paper_2506_02486_b200.emulate import run_emulated
+    import torch
+    if not all(nvls.supported(g) for g in range(NGPU)):
+        pytest.skip("no NVSwitch multicast on this box")
+    monkeypatch.setenv("DIOMP_NVLS_WINDOW", str(2 * MIB))   # rounds of <= 2 MiB (+ header)
+    k = min(NGPU, 4)
+    cases = [("f32", "sum", 3 * MIB // 4 + 5), ("f64", "sum", MIB // 8 + 3),
+             ("i32", "sum", MIB + 1), ("i32", "min", 1001), ("i64", "max", 70_001),
+             ("i64", "sum", 3), ("f32", "sum", 1)]
+
+    def contrib(r, et, count, i):
+        rng = np.random.default_rng(700 + 10 * i + r)
+        if et[0] == "f":
+            return rng.uniform(-1, 1, count).astype(DT[et])
+        return rng.integers(-2**28, 2**28, count).astype(DT[et])
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        buf = rt.alloc_symmetric(8 * MIB, 0)
+        out = rt.alloc_symmetric(8 * MIB, 0)
+        res = []
+        for i, (et, kind, count) in enumerate(cases):
+            op = coll.ReduceOp(coll.ReduceKind(kind), coll.ElementType(et))
+            v = contrib(rt.rank, et, count, i)
+            _write(rt, buf, v)
+            in_place = i % 2 == 1
+            dst = buf if in_place else out
+            coll.allreduce(comm, buf.addr, dst.addr, count, op, algorithm="nvls")
+            res.append(_read(rt, dst, DT[et], count).copy())
+            _write(rt, buf, v)
+            coll.allreduce(comm, buf.addr, out.addr, count, op)          # exact, same comm
+            res.append(_read(rt, out, DT[et], count).copy())
+        with pytest.raises(coll.TypeMismatch):
+            coll.allreduce(comm, buf.addr, out.addr, 8,
+                           coll.ReduceOp(coll.ReduceKind.Min, coll.ElementType.f32),
+                           algorithm="nvls")
+        return res
+
+    got = run_emulated(k, fn, segment_bytes=64 * MIB)
+    for i, (et, kind, count) in enumerate(cases):
+        want = O.allreduce_fold([contrib(r, et, count, i) for r in range(k)], kind)
+        for g in got:
+            nv, ex = g[2 * i], g[2 * i + 1]
+            assert ex.tobytes() == want.tobytes(), (et, kind, "exact")
+            if et[0] == "i":
+                assert nv.tobytes() == want.tobytes(), (et, kind, "nvls")
+            else:
+                tol = 1e-6 if et == "f32" else 1e-12
+                w64 = want.astype(np.float64)
+                err = np.linalg.norm(nv.astype(np.float64) - w64) / max(np.linalg.norm(w64), 1e-300)
+                assert err <= tol, (et, kind, err)
+    _ = torch
