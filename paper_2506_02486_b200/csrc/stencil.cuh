@@ -21,8 +21,8 @@
 //     come from the centre plane's slot with 16 B shared loads (conflict-free
 //     rows), interleaved tap by tap so only a sliding pair of rows is live;
 //   * u_next is stored with 16 B coalesced stores.
-// Measured (1024^3, one B200): 229 Gpts/s, DRAM traffic 1.04x the 24 B/point
-// algorithmic minimum (profiles/r01_stencil_v5_full_summary.json).
+// Measured (1024^3, one B200): 246 Gpts/s, DRAM traffic 1.04x the 24 B/point
+// algorithmic minimum (profiles/r01_stencil_v6_full_summary.json).
 // Fused driver epilogue: output planes [R,2R) / [nxl, nxl+R) are also stored
 // into the left / right neighbour's u_next ghost planes over NVLink (peer
 // pointers), the point source is added in-register (one extra rounded add,
