@@ -57,12 +57,15 @@ class BenchSpec:
     iters: int = 100
     warmup: int = 5
     transfer: TransferKind | None = None
+    allocation: str = "symmetric"   # or "asymmetric": the target is a resolved cell payload
 
     def __post_init__(self):
         if self.iters < 1:
             raise UsageError("iters must be >= 1")
         if list(self.sizes) != sorted(self.sizes):
             raise UsageError("sizes must be ascending")
+        if self.allocation not in ("symmetric", "asymmetric"):
+            raise UsageError(f"unknown allocation {self.allocation!r}")
 
 
 @dataclass
@@ -104,12 +107,16 @@ def run_p2p(rt: Runtime, spec: BenchSpec) -> list[BenchRow]:
     if rt.nranks < 2:
         raise UsageError("p2p benchmark needs at least 2 ranks")
     size_max = max(spec.sizes)
-    buf = rt.alloc_symmetric(size_max, 0)
+    asym = spec.allocation == "asymmetric"
+    # asymmetric: every rank binds a size_max payload in its asymmetric region;
+    # the initiator reaches rank 1's through the two-step access (one 32-byte
+    # cell read, then cached per generation -- runtime.py:318-349)
+    buf = rt.alloc_asymmetric(size_max, 0) if asym else rt.alloc_symmetric(size_max, 0)
     src = rt.alloc_symmetric(size_max, 0)
     rows: list[BenchRow] = []
     rt.barrier(rt.world)
     if rt.rank == 0:
-        dst = rt.translate(buf.addr, 1)
+        dst = rt.resolve_cell(buf, 1) if asym else rt.translate(buf.addr, 1)
         stats = rt.engine.stats
         timer = _Timer(rt)
         d2d = spec.transfer is TransferKind.D2D
@@ -132,7 +139,8 @@ def run_p2p(rt: Runtime, spec: BenchSpec) -> list[BenchRow]:
                 reps = _one_rep(rt, spec.kind, dst, payload, sink, size, spec.iters, d2d, src)
                 elapsed = time.perf_counter() - t0
             wire = stats.put_bytes_total() - wire0
-            rows.append(BenchRow(spec.kind.value + ("_d2d" if d2d else ""), size, reps,
+            rows.append(BenchRow(spec.kind.value + ("_d2d" if d2d else "") + ("_asym" if asym else ""),
+                                 size, reps,
                                  elapsed / reps * 1e6, size * reps / elapsed / MIB, wire))
     rt.barrier(rt.world)
     rt.free(src)
@@ -266,7 +274,7 @@ def _line(rt, metric, value, unit, args, config, extra):
 
 
 def _p2p_cli(args):
-    rt = _cli_runtime(4 << 30)
+    rt = _cli_runtime(8 << 30)   # 2 GiB symmetric + a 1 GiB asymmetric payload
     if rt.nranks < 2:
         raise UsageError("--workload p2p needs 2 GPUs (torchrun --nproc-per-node 2)")
     sizes = tuple(8 << i for i in range(28))  # 8 B .. 1 GiB
@@ -278,18 +286,33 @@ def _p2p_cli(args):
                                      transfer=TransferKind.D2D))
         out[kind.value] = [(r.size_bytes, round(r.mean_us, 3),
                             round(r.size_bytes / r.mean_us / 1e3, 2)) for r in rows]
+    # the same sweep against an asymmetric allocation (configs[1]: "symmetric
+    # and asymmetric allocations")
+    for kind in (BenchKind.Bandwidth, BenchKind.GetBandwidth, BenchKind.PutLatency,
+                 BenchKind.GetLatency):
+        szs = sizes if kind in (BenchKind.Bandwidth, BenchKind.GetBandwidth) else sizes[:11]
+        rows = run_p2p(rt, BenchSpec(kind, szs, iters=max(args.steps, 5), warmup=args.warmup,
+                                     transfer=TransferKind.D2D, allocation="asymmetric"))
+        out[kind.value + "_asym"] = [(r.size_bytes, round(r.mean_us, 3),
+                                      round(r.size_bytes / r.mean_us / 1e3, 2)) for r in rows]
     if rt.rank == 0:
         big = [gbps for n, _, gbps in out["bw"] if n >= 64 * MIB]
         value = out["bw"][-1][2]
         _line(rt, "put_bandwidth_1GiB", value, "GB/s", args,
               {"workload": "p2p_d2d_sweep_8B_1GiB", "pair": "rank0->rank1",
-               "symmetric": True},
+               "allocations": ["symmetric", "asymmetric"]},
               {"roofline": {"bound": "nvlink", "achieved": value, "peak": NVLINK_PEER_GBS,
                             "unit": "GB/s", "frac": round(value / NVLINK_PEER_GBS, 4),
                             "nominal": NVLINK_NOMINAL_GBS},
                "min_bw_ge_64MiB": min(big) if big else None,
                "get_bandwidth_1GiB": out["get_bw"][-1][2],
                "put_latency_us_8B": out["put"][0][1], "get_latency_us_8B": out["get"][0][1],
+               "asymmetric": {"put_bandwidth_1GiB": out["bw_asym"][-1][2],
+                              "get_bandwidth_1GiB": out["get_bw_asym"][-1][2],
+                              "min_put_bw_ge_64MiB": min(g for n, _, g in out["bw_asym"]
+                                                         if n >= 64 * MIB),
+                              "put_latency_us_8B": out["put_asym"][0][1],
+                              "get_latency_us_8B": out["get_asym"][0][1]},
                "rows": out, "row_format": "[bytes, mean_us, GB/s]"})
     rt.finalize()
     return 0

@@ -12,7 +12,9 @@ B200 execution (StencilRunner):
     planes + neighbour flags (csrc/stencil.cuh); the whole loop is enqueued
     with no host involvement;
   * listing1 (ranks sharing a GPU): the reference's order -- exchange()
-    puts + fence + barrier, then the update kernel -- host-synchronised.
+    puts + fence + barrier, then the update kernel -- host-synchronised;
+  * twosided (exchange="twosided"): the reference's mailbox send/recv
+    comparison variant (apps/halo_twosided.py), host-synchronised.
 """
 
 from __future__ import annotations
@@ -28,7 +30,7 @@ from .. import _native
 from ..errors import DecompositionError, UsageError
 from ..global_memory import GlobalAddress, TransferKind
 from ..runtime import COUNTER_STENCIL, Runtime
-from . import halo_onesided
+from . import halo_onesided, halo_twosided
 
 VELOCITY = 1500.0
 _COEF = (-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0)
@@ -104,9 +106,16 @@ class StencilRunner:
 
         if mode is None:
             mode = "fused" if (nranks == 1 or rt.distinct_gpus(rt.world.members)) else "listing1"
-        if mode not in ("fused", "listing1"):
+        if mode not in ("fused", "listing1", "twosided"):
             raise UsageError(f"unknown stencil mode {mode!r}")
         self.mode = mode
+        self.mailbox = None
+        if mode == "twosided":
+            mb = halo_twosided.mailbox_bytes(r, self.plane_bytes)
+            self.mailbox = rt.alloc_symmetric(mb, 0)
+            _native.call("diomp_memset_async", base + self.mailbox.addr.offset, 0, mb,
+                         self.stream.handle)
+            self.stream.synchronize()
         self.step = 0
         self.left = rt.rank - 1 if rt.rank > 0 else None
         self.right = rt.rank + 1 if rt.rank < nranks - 1 else None
@@ -167,8 +176,14 @@ class StencilRunner:
             return
         for _ in range(nsteps):
             cur = self.field_b if self.step % 2 == 0 else self.field_a
-            halo_onesided.exchange(rt, rt.world, cur.addr, self.plane_bytes, self.spec.radius,
-                                   self.nxl, rt.rank, rt.nranks, stream=None)
+            if rt.nranks > 1 and self.mode == "twosided":
+                halo_twosided.exchange(rt, rt.world, cur.addr, self.mailbox.addr,
+                                       self.plane_bytes, self.spec.radius, self.nxl, rt.rank,
+                                       rt.nranks, self.step)
+            elif rt.nranks > 1:
+                halo_onesided.exchange(rt, rt.world, cur.addr, self.plane_bytes,
+                                       self.spec.radius, self.nxl, rt.rank, rt.nranks,
+                                       stream=None)
             plan = self._plan()
             _native.check(_native.lib.diomp_stencil_run(plan, self.step, 1, self.stream.handle),
                           "stencil_run")
@@ -181,16 +196,17 @@ class StencilRunner:
         return self.field_b if self.step % 2 == 0 else self.field_a
 
     def free(self):
+        if self.mailbox is not None:
+            self.rt.free(self.mailbox)
         self.rt.free(self.field_b)
         self.rt.free(self.field_a)
 
 
 def run_stencil(rt: Runtime, spec: StencilSpec, exchange: str = "onesided",
                 gather: bool = True) -> StencilResult:
-    if exchange not in ("onesided", "fused"):
-        raise UsageError(f"exchange={exchange!r}: the two-sided mailbox variant is out of "
-                         "scope for this build (see DESIGN.md)")
-    runner = StencilRunner(rt, spec)
+    if exchange not in ("onesided", "fused", "twosided"):
+        raise UsageError(f"unknown exchange {exchange!r}")
+    runner = StencilRunner(rt, spec, "twosided" if exchange == "twosided" else None)
     rt.barrier(rt.world)
     t0 = time.perf_counter()
     runner.run(spec.steps)

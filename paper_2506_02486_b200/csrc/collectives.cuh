@@ -287,10 +287,25 @@ __global__ void __launch_bounds__(THREADS) bcast_kernel(const __grid_constant__ 
     exit_barrier(a.t);
 }
 
-static int grid_for(uint64_t work_items) {
+// CTAs per SM (512 threads each).  Measured through the C ABI
+// (tools/coll_probe.cpp, profiles/r01_collprobe_k{2,4}.txt): 2 CTAs/SM wins
+// below 256 MiB (16 MiB allreduce k=2: 399 vs 324 GB/s busBW; 64 MiB k=4:
+// 587 vs 559) and for every bcast size; 4 CTAs/SM (more loads in flight)
+// wins the large allreduces by 1-2 %.  DIOMP_COLL_CTAS_PER_SM overrides.
+static int ctas_per_sm(uint64_t bytes, bool reduce) {
+    static int env = [] {
+        const char *e = getenv("DIOMP_COLL_CTAS_PER_SM");
+        int x = e ? atoi(e) : 0;
+        return x < 0 ? 0 : (x > 4 ? 4 : x);
+    }();
+    if (env) return env;
+    return (reduce && bytes >= (256ull << 20)) ? 4 : 2;
+}
+
+static int grid_for(uint64_t work_items, int per_sm) {
     int64_t want = ceil_div((int64_t)work_items, THREADS);
     if (want < 1) want = 1;
-    if (want > kNumSMs * 4) want = kNumSMs * 4;
+    if (want > kNumSMs * per_sm) want = kNumSMs * per_sm;
     return (int)want;
 }
 
@@ -318,7 +333,7 @@ template <typename T, typename OP>
 static int launch_reduce(Args a, cudaStream_t s) {
     const uint64_t per = a.count / a.t.k + 1;
     const uint64_t items = per / (16 / sizeof(T)) + 1;
-    const int g = grid_for(items);
+    const int g = grid_for(items, ctas_per_sm(a.count * sizeof(T), true));
     const bool ce = a.mode == 0 && a.t.sync && a.t.k > 1 && a.count * sizeof(T) >= ar_ce_min();
     if (ce) a.mode = 2;
     // KMAX = smallest supported team bound >= k (register footprint, and the
@@ -426,7 +441,7 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
     a.count = nbytes;
     a.root = root;
     const uint64_t per = nbytes / (uint64_t)(team->k - 1) / 16 + 1;
-    const int g = grid_for(per);
+    const int g = grid_for(per, ctas_per_sm(nbytes, false));
     bcast_kernel<<<g, THREADS, 0, (cudaStream_t)stream>>>(a);
     DIOMP_LAUNCH_CHECK();
     return DIOMP_OK;

@@ -38,12 +38,29 @@ def test_plan_for_stencil_and_env_mapping():
     ["-n", "2", "matmul", "--n", "8", "--p", "4"],       # P = nranks * devices
     ["-n", "4", "--nodes", "5", "p2p"],
     ["-n", "2", "--node-map", "0", "p2p"],
-    ["-n", "2", "stencil", "--grid", "8", "--exchange", "twosided"],
+    ["-n", "3", "stencil", "--grid", "8", "--exchange", "twosided"],  # 3 does not divide 8
 ])
 def test_usage_errors(argv):
     with pytest.raises(UsageError):
         cli.parse_args(argv)
     assert cli.main(argv) == cli.EXIT_USAGE
+
+
+def test_twosided_exchange_accepted():
+    plan = cli.parse_args(["-n", "2", "stencil", "--grid", "8", "--exchange", "twosided"])
+    assert plan.opts["exchange"] == "twosided"
+
+
+def test_halo_loc_report():
+    """apps/loc.py (reference loc.py): effective lines of each exchange body;
+    the one-sided routine is the shorter one."""
+    from paper_2506_02486_b200.apps import loc
+    rep = loc.halo_loc_report()
+    assert 0 < rep["onesided"] < rep["twosided"]
+    src = "def exchange(a):\n    '''doc'''\n    # c\n\n    x = 1\n    return x\n"
+    assert loc.loc_metric(src) == 2
+    assert loc.effective_lines("a = 1\n# c\n\nb = 2\n") == 2
+    assert loc.effective_lines("") == 0
 
 
 def test_argparse_errors_exit_2(capsys):

@@ -71,6 +71,26 @@ def test_benchmark_accounting_and_csv():
     assert len(lines) == 3 and lines[1].startswith("put,64,5,")
 
 
+@pytest.mark.parametrize("kind", ["bw", "get_bw", "put", "get"])
+def test_p2p_bench_asymmetric_target(kind):
+    """configs[1] asymmetric leg: rank 0 reaches rank 1's asymmetric payload
+    through resolve_cell (byte exactness of asymmetric puts/gets:
+    test_gpu_rma.py)."""
+    from paper_2506_02486_b200.apps import bench as B
+    from paper_2506_02486_b200.emulate import run_emulated
+    from paper_2506_02486_b200.global_memory import TransferKind
+
+    def fn(rt):
+        spec = B.BenchSpec(B.BenchKind(kind), (8, 4096, 65536), iters=3, warmup=1,
+                           transfer=TransferKind.D2D, allocation="asymmetric")
+        rows = B.run_p2p(rt, spec)
+        return [(r.kind, r.size_bytes, r.iters) for r in rows]
+
+    out = run_emulated(2, fn, segment_bytes=4 * MIB)
+    assert out[0] == [(f"{kind}_d2d_asym", n, 3) for n in (8, 4096, 65536)]
+    assert out[1] == []
+
+
 def test_collective_bench_rows():
     from paper_2506_02486_b200.apps import bench as B
     from paper_2506_02486_b200.emulate import run_emulated

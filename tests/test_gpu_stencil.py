@@ -56,6 +56,19 @@ def test_multi_rank_decomposition_independence(key, ranks):
     assert _run(*key, ranks=ranks) == CASES[key]["sha256"]
 
 
+@pytest.mark.parametrize("key,ranks", [((16, 12, 12, 4, 1.0), 2), ((24, 20, 18, 7, 1.0), 3)])
+def test_twosided_mailbox_exchange(key, ranks):
+    """exchange="twosided" (reference halo_twosided.py): mailbox puts, delivery
+    tags, unpack -- the same field as the one-sided run, bit for bit."""
+    from paper_2506_02486_b200.apps.stencil import StencilSpec, run_stencil
+    from paper_2506_02486_b200.emulate import run_emulated
+    nx, ny, nz, steps, amp = key
+    spec = StencilSpec(nx, ny, nz, steps=steps, source_amplitude=amp)
+    out = run_emulated(ranks, lambda rt: run_stencil(rt, spec, exchange="twosided").checksum,
+                       segment_bytes=_seg_bytes(nx, ny, nz, ranks))
+    assert out[0] == CASES[key]["sha256"]
+
+
 def test_baseline_config1_128cubed_two_ranks():
     key = (128, 128, 128, 100, 1.0)
     assert _run(*key, ranks=2) == CASES[key]["sha256"]
