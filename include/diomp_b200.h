@@ -162,6 +162,12 @@ int diomp_team_barrier(const diomp_team *team, void *stream);
 #define DIOMP_MAX 2
 int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_t root,
                 void *stream);
+/* bcast algorithm switch: from `bytes` (default never; DIOMP_BCAST_CHAIN_MIN,
+ * DIOMP_BCAST_ALGO=pull|chain) device-synchronised teams of k >= 3 use the
+ * chain (root -> root+1 -> ... pipelined in chunks with per-CTA progress
+ * flags, measured slower on B200); otherwise every non-root pulls its 1/(k-1)
+ * block from the root and pushes it to the other non-roots.  Same bytes.    */
+int diomp_set_bcast_chain_min(uint64_t bytes);
 int diomp_reduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
                  int32_t dtype, int32_t op, int32_t root, void *stream);
 int diomp_set_allreduce_ce_min(uint64_t bytes);

@@ -21,6 +21,7 @@
 // cross-collective slot race of the reference cannot occur.
 #pragma once
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -287,6 +288,104 @@ __global__ void __launch_bounds__(THREADS) bcast_kernel(const __grid_constant__ 
     exit_barrier(a.t);
 }
 
+// bcast, chain algorithm (k >= 3, large buffers): positions in ring order
+// from the root form a pipeline root -> root+1 -> ... -> root+k-1.  The body
+// (16-B vectors) is cut into chunks; CTA b of every position handles chunks
+// b, b+G, b+2G, ... in order: it waits until its predecessor's CTA b has
+// delivered the chunk (a per-CTA progress flag in the own scratch), stores
+// the chunk from its own buffer into the successor's, and publishes its
+// progress in the successor's scratch.  Every NVLink link carries the buffer
+// once in one direction -- measured faster than pull+push on 4 B200
+// (tools/fanout_probe.cu: 686-694 vs 623-633 GB/s at 1 GiB, no flags).
+// With the progress flags in place it loses, though: every chunk costs its
+// CTA a system fence before the flag, and the fences dominate (4 B200, C-ABI
+// probe, profiles/r01_bcast_chain_sweep.txt: best 628 GB/s at 1 GiB with 128
+// CTAs x 256 KiB chunks vs 609 for pull+push, and 2x slower at 64 MiB).  So it
+// is opt-in (DIOMP_BCAST_ALGO=chain / diomp_set_bcast_chain_min).
+// Progress flags: chain_flags(q)[slot of the writer][b], value
+// (E << 32) | chunks delivered, E = the call's entry signal value of the pair
+// (monotone over every collective between the two endpoints, so old values
+// can never satisfy a new wait).  Unaligned head/tail bytes: the root stores
+// them to every member directly.
+constexpr int CHAIN_GMAX = 256;                     // flag slots per writer
+constexpr uint64_t CHAIN_FLAGS_OFF = 4096;          // from flag_off: after signals + counters
+constexpr int CHAIN_U = 4;
+
+__device__ __forceinline__ uint64_t *chain_flag(const diomp_team &t, int at, int writer, int b) {
+    return (uint64_t *)(t.base[at] + t.flag_off + CHAIN_FLAGS_OFF) +
+           (uint64_t)t.slot[writer] * CHAIN_GMAX + b;
+}
+
+__global__ void __launch_bounds__(THREADS) bcast_chain_kernel(const __grid_constant__ Args a,
+                                                              uint64_t chv) {
+    entry_barrier(a.t);
+    const diomp_team &t = a.t;
+    const int k = t.k, p = t.pos, root = a.root;
+    const int h = (p - root + k) % k;                 // hop distance from the root
+    const int succ = (p + 1) % k, pred = (p + k - 1) % k;
+    const uint64_t off = a.send_off, n = a.count;
+    const uint64_t al = (off + 15) & ~(uint64_t)15;
+    const uint64_t body_lo = al - off < n ? al - off : n;
+    const uint64_t nvec = (n - body_lo) / 16, body_hi = body_lo + nvec * 16;
+    const uint4 *mine = reinterpret_cast<const uint4 *>(t.base[p] + off + body_lo);
+    uint4 *next = reinterpret_cast<uint4 *>(t.base[succ] + off + body_lo);
+    const uint64_t E = (uint64_t)(t.epoch_from[pred] + 1) << 32;   // from the predecessor
+    const uint64_t Eo = (uint64_t)(t.epoch_to[succ] + 1) << 32;    // to the successor
+    const uint64_t nch = (nvec + chv - 1) / chv;
+    uint64_t i = 0;
+    // the last hop only receives (its predecessor's exit signal follows the
+    // predecessor's system fences, so the exit barrier covers the data)
+    for (uint64_t c = blockIdx.x; h < k - 1 && c < nch; c += gridDim.x, ++i) {
+        if (h > 0) {
+            if (threadIdx.x == 0) wait_ge(chain_flag(t, p, pred, blockIdx.x), E | (i + 1));
+            __syncthreads();
+        }
+        const uint64_t lo = c * chv, hi = lo + chv < nvec ? lo + chv : nvec;
+        uint64_t v = lo + threadIdx.x;
+        // L2-only loads: the chunk was just written over NVLink by the predecessor
+        for (; v + (CHAIN_U - 1) * THREADS < hi; v += CHAIN_U * THREADS) {
+            uint4 r[CHAIN_U];
+#pragma unroll
+            for (int u = 0; u < CHAIN_U; ++u) r[u] = __ldcg(mine + v + u * THREADS);
+#pragma unroll
+            for (int u = 0; u < CHAIN_U; ++u) next[v + u * THREADS] = r[u];
+        }
+        for (; v < hi; v += THREADS) next[v] = __ldcg(mine + v);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            st_release_sys(chain_flag(t, succ, p, blockIdx.x), Eo | (i + 1));
+        }
+    }
+    if (h == 0 && blockIdx.x == 0) {   // unaligned head / tail bytes straight from the root
+        const uint8_t *s8 = reinterpret_cast<const uint8_t *>(t.base[root] + off);
+        const uint64_t ntail = n - body_hi;
+        for (uint64_t e0 = threadIdx.x; e0 < body_lo + ntail; e0 += THREADS) {
+            const uint64_t e = e0 < body_lo ? e0 : body_hi + (e0 - body_lo);
+            const uint8_t b = s8[e];
+            for (int q = 0; q < k; ++q)
+                if (q != root) reinterpret_cast<uint8_t *>(t.base[q] + off)[e] = b;
+        }
+    }
+    exit_barrier(a.t);
+}
+
+// bcast algorithm: chain for k >= 3 from DIOMP_BCAST_CHAIN_MIN bytes (default
+// never, see above), else pull+push.  DIOMP_BCAST_ALGO=pull|chain forces one.
+static std::atomic<uint64_t> g_bcast_chain_min{~0ull};
+static std::once_flag g_bc_once;
+
+static uint64_t bcast_chain_min() {
+    std::call_once(g_bc_once, [] {
+        const char *algo = getenv("DIOMP_BCAST_ALGO");
+        const char *e = getenv("DIOMP_BCAST_CHAIN_MIN");
+        if (e) g_bcast_chain_min = (uint64_t)strtoull(e, nullptr, 10);
+        if (algo && !strcmp(algo, "pull")) g_bcast_chain_min = ~0ull;
+        if (algo && !strcmp(algo, "chain")) g_bcast_chain_min = 0;
+    });
+    return g_bcast_chain_min.load(std::memory_order_relaxed);
+}
+
 // CTAs per SM (512 threads each).  Measured through the C ABI
 // (tools/coll_probe.cpp, profiles/r01_collprobe_k{2,4}.txt): 2 CTAs/SM wins
 // below 256 MiB (16 MiB allreduce k=2: 399 vs 324 GB/s busBW; 64 MiB k=4:
@@ -397,6 +496,12 @@ int diomp_set_allreduce_ce_min(uint64_t bytes) {
     return DIOMP_OK;
 }
 
+int diomp_set_bcast_chain_min(uint64_t bytes) {
+    diomp::coll::bcast_chain_min();  // settle the environment default first
+    diomp::coll::g_bcast_chain_min.store(bytes, std::memory_order_relaxed);
+    return DIOMP_OK;
+}
+
 int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
                     int32_t dtype, int32_t op, void *stream) {
     using namespace diomp::coll;
@@ -440,6 +545,25 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
     a.recv_off = offset;
     a.count = nbytes;
     a.root = root;
+    if (team->sync && team->k >= 3 && nbytes >= bcast_chain_min() && nbytes >= 16 * CHAIN_GMAX) {
+        // chunk / CTA count: DIOMP_BCAST_CHAIN_CHUNK (bytes), DIOMP_BCAST_CHAIN_G
+        static const uint64_t env_chunk = [] {
+            const char *e = getenv("DIOMP_BCAST_CHAIN_CHUNK");
+            return e ? (uint64_t)strtoull(e, nullptr, 10) : (uint64_t)(256 << 10);
+        }();
+        static const int env_g = [] {
+            const char *e = getenv("DIOMP_BCAST_CHAIN_G");
+            int x = e ? atoi(e) : 128;
+            return x < 1 ? 1 : (x > CHAIN_GMAX ? CHAIN_GMAX : x);
+        }();
+        const uint64_t nvec = nbytes / 16;
+        const uint64_t chv = std::max<uint64_t>(env_chunk / 16, 32);
+        const uint64_t nch = (nvec + chv - 1) / chv;
+        const int g = (int)std::min<uint64_t>((uint64_t)env_g, nch);
+        bcast_chain_kernel<<<g, THREADS, 0, (cudaStream_t)stream>>>(a, chv);
+        DIOMP_LAUNCH_CHECK();
+        return DIOMP_OK;
+    }
     const uint64_t per = nbytes / (uint64_t)(team->k - 1) / 16 + 1;
     const int g = grid_for(per, ctas_per_sm(nbytes, false));
     bcast_kernel<<<g, THREADS, 0, (cudaStream_t)stream>>>(a);

@@ -146,6 +146,48 @@ def test_device_flag_mode_back_to_back():
         assert all(r[rep] == want for r in res)
 
 
+@need_gpus(3)
+def test_bcast_chain_device_flags():
+    """Chain bcast (k >= 3, per-CTA progress flags): every member ends with
+    the root's bytes -- odd sizes and offsets, every root, repeated, mixed with
+    pull+push bcasts and allreduces so the progress-flag values must stay
+    monotone across calls and algorithms."""
+    from paper_2506_02486_b200 import GlobalAddress, _native
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200.emulate import run_emulated
+    k = min(NGPU, 4)
+    plan = [(4096 + 5, 0, 0), (MIB + 7, 1, 0), (24 * MIB + 13, 2, 0), (777, 0, 1 << 62),
+            (3 * MIB, k - 1, 0), (24 * MIB + 13, 0, 0), (5 * MIB + 1, 1, 1 << 62),
+            (24 * MIB + 13, k - 1, 0)]
+    op = coll.ReduceOp(coll.ReduceKind.Sum, coll.ElementType.i32)
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        assert comm.device_sync
+        buf = rt.alloc_symmetric(32 * MIB, 0)
+        acc = rt.alloc_symmetric(4096, 0)
+        out = []
+        for i, (size, root, chain_min) in enumerate(plan):
+            _native.call("diomp_set_bcast_chain_min", chain_min)
+            mine = np.random.default_rng(7000 + 13 * i + rt.rank).integers(0, 256, size,
+                                                                           dtype=np.uint8)
+            at = GlobalAddress(rt.rank, 0, buf.addr.offset + 3)
+            rt.gm.view(0, at.offset, size)[:] = mine.tobytes()
+            coll.bcast(comm, at, size, root=root)
+            out.append((mine.tobytes() if rt.rank == root else None,
+                        bytes(rt.gm.view(0, at.offset, size))))
+            coll.allreduce(comm, acc.addr, acc.addr, 1000, op)
+        return out
+
+    try:
+        res = run_emulated(k, fn, segment_bytes=128 * MIB)
+    finally:
+        _native.call("diomp_set_bcast_chain_min", (1 << 64) - 1)
+    for i in range(len(plan)):
+        snap = next(r[i][0] for r in res if r[i][0] is not None)
+        assert all(r[i][1] == snap for r in res), i
+
+
 @need_gpus(2)
 @pytest.mark.parametrize("ce_min", [None, 8 * MIB])
 def test_allreduce_device_flag_algorithms_bitwise(ce_min):

@@ -26,7 +26,7 @@ int main(int argc, char **argv) {
     if (argc > 2) K = atoi(argv[2]);
     const bool ar = !strcmp(op, "allreduce");
     const uint64_t NMAX = 1ull << 30, SEG = 2 * NMAX + (64ull << 20);
-    const uint64_t SEND = 0, RECV = NMAX, FLAG = 2 * NMAX, CNT = FLAG + 4096;
+    const uint64_t SEND = 0, RECV = NMAX, FLAG = 2 * NMAX, CNT = FLAG + 512;  // the runtime's scratch layout
     std::vector<uint64_t> base(K);
     std::vector<void *> st(K);
     for (int g = 0; g < K; ++g) {

@@ -36,6 +36,44 @@ __global__ void __launch_bounds__(512) fan_store(Dst D, const uint4 *__restrict_
     }
 }
 
+// bcast data patterns on non-root p (no flags, timing only), block j = p-1:
+//   mode 0 (library today): pull block j from the root, push it to the other non-roots
+//   mode 1 (pull-only):     pull block j from the root, pull every other block b from non-root b
+//   mode 2 (push-only):     the root stores block j into non-root j; non-root j stores its
+//                           (local) block into the other non-roots
+struct Team { char *b[8]; };
+__global__ void __launch_bounds__(512) bc_pattern(Team T, int k, int p, uint64_t per16, int mode) {
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = p - 1;
+    if (mode == 0) {
+        const uint4 *src = (const uint4 *)T.b[0] + j * per16;
+        for (uint64_t i = g; i < per16; i += gs) {
+            uint4 v = src[i];
+            for (int q = 1; q < k; ++q) ((uint4 *)T.b[q])[j * per16 + i] = v;
+        }
+    } else if (mode == 3) {  // chain: position p stores the whole buffer into p+1
+        const uint64_t n = per16 * (k - 1);
+        if (p + 1 < k)
+            for (uint64_t i = g; i < n; i += gs) ((uint4 *)T.b[p + 1])[i] = ((const uint4 *)T.b[p])[i];
+    } else if (mode == 2) {
+        const uint4 *src = (const uint4 *)T.b[p] + j * per16;
+        for (uint64_t i = g; i < per16; i += gs) {
+            uint4 v = src[i];
+            for (int q = 1; q < k; ++q) if (q != p) ((uint4 *)T.b[q])[j * per16 + i] = v;
+        }
+    } else {
+        // CTA slices: 1/(k-1) of the grid for the own block, the rest for peer blocks
+        const uint64_t items = per16 * (k - 1);
+        for (uint64_t i = g; i < items; i += gs) {
+            const int bi = (int)(i / per16);          // block index 0..k-2
+            const uint64_t e = i - bi * per16;
+            const int srcpos = bi == j ? 0 : bi + 1;  // own block from the root, others from their owner
+            ((uint4 *)T.b[p])[bi * per16 + e] = ((const uint4 *)T.b[srcpos])[bi * per16 + e];
+        }
+    }
+}
+
 int main(int argc, char **argv) {
     int K; CK(cudaGetDeviceCount(&K));
     const uint64_t S = 1ull << 30;
@@ -50,6 +88,7 @@ int main(int argc, char **argv) {
         for (auto &s : st[g]) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     }
     for (uint64_t sz : {64ull << 20, 256ull << 20, 1ull << 30}) {
+        if (getenv("SKIP_FANOUT")) break;
         const uint64_t per = sz / (K - 1) / 16 * 16;
         for (int v = 0; v < 4; ++v) {
             for (int ctas : {296, 592}) {
@@ -76,6 +115,28 @@ int main(int argc, char **argv) {
                        (unsigned long long)(sz >> 20), (double)per * (K - 1) / t / 1e9);
                 fflush(stdout);
             }
+        }
+    }
+    for (uint64_t sz : {64ull << 20, 256ull << 20, 1ull << 30}) {
+        const uint64_t per = sz / (K - 1) / 16 * 16;
+        Team T{}; for (int g = 0; g < K; ++g) T.b[g] = buf[g];
+        for (int mode = 0; mode < 4; ++mode) for (int ctas : {296, 592}) {
+            if (mode == 1 || mode == 2) continue;
+            auto run = [&] {
+                if (mode == 2) { CK(cudaSetDevice(0)); Dst D{}; for (int g = 1; g < K; ++g) D.d[g - 1] = (uint4 *)(buf[g] + (g - 1) * per);
+                    fan_store<<<ctas, 512, 0, st[0][0]>>>(D, (const uint4 *)buf[0], per / 16, K - 1); }
+                for (int g = mode == 3 ? 0 : 1; g < K; ++g) { CK(cudaSetDevice(g));
+                bc_pattern<<<ctas, 512, 0, st[g][0]>>>(T, K, g, per / 16, mode); } };
+            auto sync = [&] { for (int g = 0; g < K; ++g) { CK(cudaSetDevice(g)); CK(cudaDeviceSynchronize()); } };
+            run(); sync();
+            const int reps = sz >= (256ull << 20) ? 10 : 30;
+            auto t0 = std::chrono::steady_clock::now();
+            for (int r = 0; r < reps; ++r) run();
+            sync();
+            double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
+            printf("K=%d bcast-pattern %-9s ctas=%3d %5llu MiB  S/t %6.1f GB/s\n", K, mode == 3 ? "chain" : mode == 2 ? "push-only" : mode ? "pull-only" : "pull+push",
+                   ctas, (unsigned long long)(sz >> 20), (double)per * (K - 1) / t / 1e9);
+            fflush(stdout);
         }
     }
     return 0;
