@@ -153,6 +153,18 @@ def _load_ref_core():
     raise ImportError("oracle/_ref/_core*.so not built")
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 class CpuReference:
     """The reference's compiled stencil_update (oracle/_ref, built from
     reference/pkg/src/diomp/kernels/_core.c with -O3 -ffp-contract=off) on
@@ -179,6 +191,7 @@ class CpuReference:
 
     def describe(self, value: float, steps: int) -> dict:
         return {"value": round(value, 4), "unit": "Gpts/s", "cores": self.cores, "kind": self.kind,
+                "cpu_model": _cpu_model(),
                 "sample": f"{self.cores} processes x {steps} steps of a "
                           f"{self.planes}x{self.grid}x{self.grid} slab each (reference "
                           f"stencil_update, aggregate over cores)"}
