@@ -391,15 +391,78 @@ def _dgemm_cli(args):
         ring.synchronize()
     got = rt.ctrl.allgather(tuple(range(rt.nranks)), "gemmbench", pickle.dumps(min(ms)))
     t = max(pickle.loads(b) for _, b in got) / 1e3
+    ring.release()
+    # library reference point: cuBLAS DGEMM (torch addmm, f64) over the same
+    # per-endpoint shapes -- P products C(ns x n) += A(ns x ns) @ B(ns x n) --
+    # without the stripe shift
+    t_cublas = _cublas_same_shapes(rt, spec, args)
+    got = rt.ctrl.allgather(tuple(range(rt.nranks)), "gemmbench/cublas", pickle.dumps(t_cublas))
+    t_cublas = max(pickle.loads(b) for _, b in got)
     if rt.rank == 0:
         tflops = 2.0 * n ** 3 / t / 1e12
+        extra = {"ms_per_multiply": round(t * 1e3, 3),
+                 "cublas_same_shapes": {"tflops": round(2.0 * n ** 3 / t_cublas / 1e12, 3),
+                                        "ms_per_multiply": round(t_cublas * 1e3, 3),
+                                        "note": "torch.addmm f64 (cuBLAS DGEMM), P products "
+                                                "per endpoint, no ring shift"},
+                 "roofline": {"bound": "tensor (DMMA f64)", "achieved": round(tflops / rt.nranks, 3),
+                              "peak": round(2.0 * n ** 3 / t_cublas / 1e12 / rt.nranks, 3),
+                              "unit": "TFLOP/s per GPU",
+                              "frac": round(t_cublas / t, 4),
+                              "peak_source": "cuBLAS DGEMM on the same shapes, this run"}}
+        if rt.nranks == 1 and os.environ.get("BENCH_GEMM_CPU", "1") != "0":
+            extra["cpu_baseline"] = _cpu_dgemm_sample(n)
         _line(rt, "dgemm_ring_tflops", round(tflops, 3), "TFLOP/s", args,
               {"workload": f"cannon_ring_{n}^2_fp64", "endpoints": rt.nranks,
-               "kernel": "DMMA m8n8k4 + fused stripe shift"},
-              {"ms_per_multiply": round(t * 1e3, 3)})
-    ring.release()
+               "kernel": "DMMA m8n8k4 + fused stripe shift"}, extra)
     rt.finalize()
     return 0
+
+
+def _cublas_same_shapes(rt, spec, args) -> float:
+    import torch
+    ns, n = spec.ns, spec.n
+    dev = torch.device("cuda", rt.gpus[0])
+    a = torch.rand(ns, n, dtype=torch.float64, device=dev)
+    b = torch.rand(ns, n, dtype=torch.float64, device=dev)
+    c = torch.zeros(ns, n, dtype=torch.float64, device=dev)
+
+    def one():
+        for s in range(spec.p):
+            c.addmm_(a[:, s * ns:(s + 1) * ns], b)
+    one()
+    torch.cuda.synchronize(dev)
+    best = float("inf")
+    for _ in range(max(args.steps, 1)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        one()
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    del a, b, c
+    torch.cuda.empty_cache()
+    return best
+
+
+def _cpu_dgemm_sample(n: int) -> dict:
+    """The reference's compute (cannon.py:138, numpy @ -> OpenBLAS) on the
+    host cores: one ring step of the P=16 split, C(1024 x n) += A(1024 x 1024)
+    @ B(1024 x n), best of 3."""
+    ns = 1024
+    rng = np.random.default_rng(0)
+    a = rng.uniform(-1, 1, (ns, ns))
+    b = rng.uniform(-1, 1, (ns, n))
+    c = np.zeros((ns, n))
+    best = float("inf")
+    for _ in range(3):
+        t0 = time.perf_counter()
+        c += a @ b
+        best = min(best, time.perf_counter() - t0)
+    return {"value": round(2.0 * ns * ns * n / best / 1e12, 4), "unit": "TFLOP/s",
+            "cores": os.cpu_count(), "kind": "reference",
+            "sample": f"numpy/OpenBLAS C += A @ B, {ns}x{ns} @ {ns}x{n} (one ring step "
+                      f"at P=16), default BLAS threads"}
 
 
 def cli_bench(args) -> int:
