@@ -346,7 +346,10 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
     // 88 % active vs cuBLAS 96.5 % (profiles/r01_dgemm_dmma_pipe.json).  The
     // single-k layout measured 0.91, cuBLAS's own 64x128 / 32x64-warp shape
     // 0.91-0.93, the 1-CTA 64x32 variants 0.86-0.87, BK=32 0.89, 4 stages at
-    // 1 CTA/SM 0.74.
+    // 1 CTA/SM 0.74.  A CUTLASS-style mainloop (next k-step's fragments
+    // loaded while the current DMMAs issue, tile boundary crossed before the
+    // last step's DMMAs) measured 0.76 (spills at 128 regs) / 0.78 (BK=32,
+    // 1 CTA/SM) / 0.90 (64x128 CTA) -- the compiler's own schedule is better.
     const char *v = getenv("DIOMP_DGEMM_CFG");
     if (v && atoi(v) == 0) return launch_dgemm<CfgBig>(p, x->device, (cudaStream_t)stream);
     if (v && atoi(v) == 1) return launch_dgemm<CfgDual>(p, x->device, (cudaStream_t)stream);
