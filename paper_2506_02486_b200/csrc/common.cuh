@@ -60,15 +60,25 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
 }
 
 // Spin until *flag >= value (system scope acquire).  Returns false on timeout.
+// Tight polling for the first DIOMP_SPIN_NS (cross-GPU flags land within a
+// few microseconds of each other in back-to-back collectives and stencil
+// steps; a sleeping poller adds up to its sleep to every handshake), then an
+// exponential nanosleep backoff.
+#ifndef DIOMP_SPIN_NS
+#define DIOMP_SPIN_NS 20000
+#endif
 __device__ __forceinline__ bool wait_ge(const uint64_t *flag, uint64_t value) {
     if (ld_acquire_sys(flag) >= value) return true;
-    uint64_t t0 = globaltimer_ns();
-    uint64_t limit = g_wait_timeout_ns;
-    unsigned ns = 32;
+    const uint64_t t0 = globaltimer_ns();
+    const uint64_t limit = g_wait_timeout_ns;
+    unsigned ns = 64;
     while (ld_acquire_sys(flag) < value) {
-        __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
-        if (globaltimer_ns() - t0 > limit) {
+        const uint64_t dt = globaltimer_ns() - t0;
+        if (dt > DIOMP_SPIN_NS) {
+            __nanosleep(ns);
+            if (ns < 1024) ns <<= 1;
+        }
+        if (dt > limit) {
             record_device_error((unsigned)DIOMP_INTERNAL);
             return false;
         }
