@@ -195,6 +195,13 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
         constexpr int C = (J + 5) % 9;  // centre bank
         const double *cr = sm + sc * SLOT + ln.so;
         double acc[4];
+#ifdef DIOMP_STENCIL_MEMONLY
+        // experiment build: same loads / barriers / stores, no taps
+#pragma unroll
+        for (int pt = 0; pt < 4; ++pt) acc[pt] = Q[C][pt] + cr[pt & 1];
+        if (false)
+#endif
+        {
 #pragma unroll
         for (int pt = 0; pt < 4; ++pt) acc[pt] = __dmul_rn(p.c0, Q[C][pt]);
 #pragma unroll
@@ -227,6 +234,7 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
             c0 = tap(c0, p.wz[2], p23.x, m21.x); c1 = tap(c1, p.wz[2], p23.y, m21.y);
             c0 = tap(c0, p.wz[3], p23.y, m43.y); c1 = tap(c1, p.wz[3], p45.x, m21.x);
             c0 = tap(c0, p.wz[4], p45.x, m43.x); c1 = tap(c1, p.wz[4], p45.y, m43.y);
+        }
         }
         // u_prev of this output plane from its TMA-filled tile, then free the tile
         const int o = q - 2 * R;
