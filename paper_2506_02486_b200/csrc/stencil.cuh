@@ -456,9 +456,18 @@ static int make_plane_map(CUtensorMap *map, const double *u, int64_t NX, int64_t
     cuuint64_t strides[2] = {(cuuint64_t)NZ * 8, (cuuint64_t)NY * NZ * 8};
     cuuint32_t box[3] = {halo ? (cuuint32_t)BZ : (cuuint32_t)TZ, halo ? (cuuint32_t)BY : (cuuint32_t)TY, 1};
     cuuint32_t estr[3] = {1, 1, 1};
+    // L2 promotion of the TMA fills (DIOMP_STENCIL_L2PROMO=0/64/128/256, default 256)
+    static const CUtensorMapL2promotion promo = [] {
+        const char *e = getenv("DIOMP_STENCIL_L2PROMO");
+        const int v = e ? atoi(e) : 256;
+        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+               : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+               : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                          : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }();
     CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)u, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? DIOMP_OK : DIOMP_BAD_REQUEST;
 }
 
