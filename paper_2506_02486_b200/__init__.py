@@ -21,6 +21,7 @@ from .streams import Stream, StreamEvent, StreamPool
 from .runtime import (CompletionHandle, Group, HandleState, Runtime, StreamedHandle, finalize,
                       init)
 from . import collectives, kernels
+from .wire import Status
 from .collectives import (Communicator, ElementType, ReduceKind, ReduceOp, UniqueId, allreduce,
                           bcast, bootstrap, device_bcast, reduce)
 

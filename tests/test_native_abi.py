@@ -77,3 +77,13 @@ def test_product_path_has_no_oracle_dependency():
                 text = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle|liboracle|oracle/", text,
                                      flags=re.M), f
+
+
+def test_wire_status_codes_match_the_c_abi():
+    """wire.Status (reference wire.py:46-52) = the library's status codes."""
+    import re
+    from paper_2506_02486_b200 import Status
+    hdr = open(os.path.join(ROOT, "include", "diomp_b200.h")).read()
+    for name in ("OK", "INVALID_ADDRESS", "BAD_REQUEST", "INTERNAL"):
+        m = re.search(rf"#define DIOMP_{name} (\d+)", hdr)
+        assert m and int(m.group(1)) == Status[name].value
