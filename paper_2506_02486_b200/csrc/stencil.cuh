@@ -27,8 +27,9 @@
 // into the left / right neighbour's u_next ghost planes over NVLink (peer
 // pointers), the point source is added in-register (one extra rounded add,
 // exactly like stencil.py:124-125), and with sync on, edge CTAs wait for the
-// neighbours' "previous step done" flag while the last CTA to finish signals
-// both neighbours -- the device-side replacement of fence+barrier.
+// neighbours' "previous step done" flag, which block 0 of each step's kernel
+// raises for the step before it (kernel order makes that step's stores
+// complete) -- the device-side replacement of fence+barrier.
 #pragma once
 
 #include <cuda.h>
@@ -320,6 +321,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
+        // this step's kernel started, so the previous step's kernel -- its
+        // u_next stores and its halo stores into the neighbours -- has
+        // completed: block 0 tells both neighbours (the previous step's
+        // completion signal, sent here instead of by a last-CTA count at the
+        // end of every step, which cost each CTA a fence and an atomic)
+        if (p.sync && blockIdx.x == 0 && (p.sig_l || p.sig_r)) {
+            __threadfence_system();
+            if (p.sig_l) st_release_sys(p.sig_l, p.sl);
+            if (p.sig_r) st_release_sys(p.sig_r, p.sr);
+        }
         if (p.sync) {
             if (xa < 2 * R && p.wait_l) wait_ge(p.wait_l, p.wl);
             if (xb > p.NX - 2 * R && p.wait_r) wait_ge(p.wait_r, p.wr);
@@ -385,11 +396,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         else consume<false>(p, sm, full, empty, psm, pfull, pempty, ln, L);
     }
 
-    const bool wrote_peer = (xa < 2 * R && p.left_next) || (xb > p.NX - 2 * R && p.right_next);
-    if (p.sync && last_cta_done(p.counter, gridDim.x, wrote_peer) && threadIdx.x == 0) {
-        if (p.sig_l) st_release_sys(p.sig_l, p.sl);
-        if (p.sig_r) st_release_sys(p.sig_r, p.sr);
-    }
 }
 
 // Generic path: any radius <= 8, any even/odd extents, no alignment needs.
@@ -658,19 +664,31 @@ int diomp_stencil_run(const diomp_stencil_plan *pl, int64_t step0, int64_t nstep
             p.amp = pl->amp;
             p.sync = pl->sync;
             p.edge_first = edge_first;
-            if (pl->sync) {
+            if (p.sync) {
                 p.wait_l = pl->left_field[pb] ? (const uint64_t *)pl->wait_left : nullptr;
                 p.wait_r = pl->right_field[pb] ? (const uint64_t *)pl->wait_right : nullptr;
                 p.wl = pl->from_left + k;     // left finished step st-1
                 p.wr = pl->from_right + k;
-                p.sig_l = pl->left_field[pb] ? (uint64_t *)pl->sig_left : nullptr;
-                p.sig_r = pl->right_field[pb] ? (uint64_t *)pl->sig_right : nullptr;
-                p.sl = pl->to_left + k + 1;
-                p.sr = pl->to_right + k + 1;
+                // completion of step st-1 (the first step of this call has
+                // nothing to announce: the previous call's trailing signal did)
+                if (k > 0) {
+                    p.sig_l = pl->left_field[pb] ? (uint64_t *)pl->sig_left : nullptr;
+                    p.sig_r = pl->right_field[pb] ? (uint64_t *)pl->sig_right : nullptr;
+                }
+                p.sl = pl->to_left + k;
+                p.sr = pl->to_right + k;
                 p.counter = (unsigned int *)pl->counter;
             }
             int rc = launch_fast(maps[cb], pmaps[pb], p, s);
             if (rc) return rc;
+            if (p.sync && st == step0 + nsteps - 1) {
+                // the last step's completion: a one-thread kernel behind it
+                if (pl->left_field[pb])
+                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_left, pl->to_left + k + 1);
+                if (pl->right_field[pb])
+                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_right, pl->to_right + k + 1);
+                DIOMP_LAUNCH_CHECK();
+            }
         } else {
             // Listing-1 order: halo puts, flag exchange, update (+ source).
             const uint64_t cur = pl->field[cb];
