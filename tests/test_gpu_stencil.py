@@ -84,6 +84,34 @@ def test_fused_device_flag_mode(key, ranks):
     assert _run(*key, ranks=ranks, mode="fused") == CASES[key]["sha256"]
 
 
+@need_gpus(2)
+def test_fused_mode_across_several_run_calls():
+    """Steps split over several runner calls (the previous call's trailing
+    completion flag must release the next call's first step): 24x20x18 as
+    2 + 1 + 4 steps equals the 7-step reference checksum, twice in a row."""
+    import hashlib
+    from paper_2506_02486_b200.apps.stencil import StencilRunner, StencilSpec, _gather_field, dump_bytes
+    from paper_2506_02486_b200.emulate import run_emulated
+    key = (24, 20, 18, 7, 1.0)
+    spec = StencilSpec(24, 20, 18, steps=7, source_amplitude=1.0)
+
+    def fn(rt):
+        out = []
+        for _ in range(2):
+            r = StencilRunner(rt, spec, mode="fused")
+            rt.barrier(rt.world)
+            for n in (2, 1, 4):
+                r.run(n)
+            rt.barrier(rt.world)
+            f = _gather_field(rt, r.cur_rec, spec, r.nxl, r.shape)
+            out.append(hashlib.sha256(dump_bytes(f)).hexdigest() if rt.rank == 0 else "")
+            r.free()
+        return out
+
+    res = run_emulated(2, fn, segment_bytes=_seg_bytes(24, 20, 18, 2))[0]
+    assert res == [CASES[key]["sha256"]] * 2
+
+
 @pytest.mark.parametrize("name", ["s4", "s4b", "s2", "s3"])
 def test_stencil_update_seam_bitwise(name):
     import torch
