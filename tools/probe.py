@@ -29,17 +29,19 @@ def _time(fn, iters=10, warm=3):
     return e0.elapsed_time(e1) / iters
 
 
-def dgemm(n=8192):
+def dgemm(n=8192, nn=None, k=None):
+    """C(n x nn) += A(n x k) @ B(k x nn); square when only n is given."""
     import torch
 
     from paper_2506_02486_b200 import gemm
-    A = torch.rand(n, n, dtype=torch.float64, device="cuda")
-    B = torch.rand(n, n, dtype=torch.float64, device="cuda")
-    C = torch.zeros(n, n, dtype=torch.float64, device="cuda")
+    nn, k = nn or n, k or n
+    A = torch.rand(n, k, dtype=torch.float64, device="cuda")
+    B = torch.rand(k, nn, dtype=torch.float64, device="cuda")
+    C = torch.zeros(n, nn, dtype=torch.float64, device="cuda")
     ms = _time(lambda: gemm.dgemm_accumulate(A, B, C), iters=5, warm=2)
-    ms_cublas = _time(lambda: torch.matmul(A, B), iters=5, warm=2)
-    fl = 2.0 * n ** 3
-    return {"probe": "dgemm", "n": n, "dmma_ms": ms, "dmma_tflops": fl / ms / 1e9,
+    ms_cublas = _time(lambda: C.addmm_(A, B), iters=5, warm=2)
+    fl = 2.0 * n * nn * k
+    return {"probe": "dgemm", "m_n_k": [n, nn, k], "dmma_ms": ms, "dmma_tflops": fl / ms / 1e9,
             "cublas_ms": ms_cublas, "cublas_tflops": fl / ms_cublas / 1e9,
             "frac_of_cublas": ms_cublas / ms}
 
