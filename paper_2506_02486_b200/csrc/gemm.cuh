@@ -350,6 +350,7 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
     // loaded while the current DMMAs issue, tile boundary crossed before the
     // last step's DMMAs) measured 0.76 (spills at 128 regs) / 0.78 (BK=32,
     // 1 CTA/SM) / 0.90 (64x128 CTA) -- the compiler's own schedule is better.
+    // 16 warps of 32x32 in a 128x128 CTA (4 stages, 1 CTA/SM): 0.81-0.83.
     const char *v = getenv("DIOMP_DGEMM_CFG");
     if (v && atoi(v) == 0) return launch_dgemm<CfgBig>(p, x->device, (cudaStream_t)stream);
     if (v && atoi(v) == 1) return launch_dgemm<CfgDual>(p, x->device, (cudaStream_t)stream);
