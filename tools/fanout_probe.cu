@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -121,7 +122,7 @@ int main(int argc, char **argv) {
         const uint64_t per = sz / (K - 1) / 16 * 16;
         Team T{}; for (int g = 0; g < K; ++g) T.b[g] = buf[g];
         for (int mode = 0; mode < 4; ++mode) for (int ctas : {296, 592}) {
-            if (mode == 1 || mode == 2) continue;
+            if (mode == 1 || mode == 2 || ctas == 296) continue;
             auto run = [&] {
                 if (mode == 2) { CK(cudaSetDevice(0)); Dst D{}; for (int g = 1; g < K; ++g) D.d[g - 1] = (uint4 *)(buf[g] + (g - 1) * per);
                     fan_store<<<ctas, 512, 0, st[0][0]>>>(D, (const uint4 *)buf[0], per / 16, K - 1); }
@@ -137,6 +138,45 @@ int main(int argc, char **argv) {
             printf("K=%d bcast-pattern %-9s ctas=%3d %5llu MiB  S/t %6.1f GB/s\n", K, mode == 3 ? "chain" : mode == 2 ? "push-only" : mode ? "pull-only" : "pull+push",
                    ctas, (unsigned long long)(sz >> 20), (double)per * (K - 1) / t / 1e9);
             fflush(stdout);
+        }
+    }
+    // copy-engine bcast pattern, all dependencies local: non-root j gets its
+    // block from the root chunk by chunk (stream 0) and, per chunk, pushes it to
+    // the other non-roots (one stream per destination) after an event
+    if (K >= 3) {
+        std::vector<std::vector<cudaEvent_t>> ev(K);
+        for (int g = 1; g < K; ++g) { CK(cudaSetDevice(g)); ev[g].resize(64);
+            for (auto &evx : ev[g]) CK(cudaEventCreateWithFlags(&evx, cudaEventDisableTiming)); }
+        for (uint64_t sz : {64ull << 20, 256ull << 20, 1ull << 30}) {
+            const uint64_t per = sz / (K - 1) / 16 * 16;
+            for (uint64_t ch : {8ull << 20, 16ull << 20, 32ull << 20, 64ull << 20}) {
+                auto run = [&] {
+                    for (int g = 1; g < K; ++g) {
+                        CK(cudaSetDevice(g));
+                        const uint64_t base = (g - 1) * per;
+                        int c = 0;
+                        for (uint64_t o = 0; o < per; o += ch, ++c) {
+                            const uint64_t len = std::min(ch, per - o);
+                            CK(cudaMemcpyAsync(buf[g] + base + o, buf[0] + base + o, len, cudaMemcpyDeviceToDevice, st[g][0]));
+                            CK(cudaEventRecord(ev[g][c % 64], st[g][0]));
+                            for (int q = 1; q < K; ++q) if (q != g) {
+                                CK(cudaStreamWaitEvent(st[g][q], ev[g][c % 64], 0));
+                                CK(cudaMemcpyAsync(buf[q] + base + o, buf[g] + base + o, len, cudaMemcpyDeviceToDevice, st[g][q]));
+                            }
+                        }
+                    }
+                };
+                auto sync = [&] { for (int g = 0; g < K; ++g) { CK(cudaSetDevice(g)); CK(cudaDeviceSynchronize()); } };
+                run(); sync();
+                const int reps = sz >= (256ull << 20) ? 10 : 30;
+                auto t0 = std::chrono::steady_clock::now();
+                for (int r = 0; r < reps; ++r) run();
+                sync();
+                double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
+                printf("K=%d bcast-pattern ce-get+ce-push chunk=%2llu MiB %5llu MiB  S/t %6.1f GB/s\n", K,
+                       (unsigned long long)(ch >> 20), (unsigned long long)(sz >> 20), (double)per * (K - 1) / t / 1e9);
+                fflush(stdout);
+            }
         }
     }
     return 0;
