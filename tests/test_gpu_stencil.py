@@ -49,7 +49,8 @@ def test_single_rank_matches_reference_checksum(key):
 
 
 @pytest.mark.parametrize("key,ranks", [((16, 12, 12, 4, 1.0), 2), ((24, 20, 18, 7, 1.0), 3),
-                                       ((20, 15, 13, 5, 1.0), 2), ((64, 64, 64, 100, 1.0), 4)])
+                                       ((20, 15, 13, 5, 1.0), 2), ((64, 64, 64, 100, 1.0), 4),
+                                       ((64, 64, 64, 100, 1.0), 8)])
 def test_multi_rank_decomposition_independence(key, ranks):
     """Emulated ranks (host-synchronised Listing-1 mode when they share a GPU,
     fused device-flag mode when each has its own)."""
@@ -67,6 +68,27 @@ def test_twosided_mailbox_exchange(key, ranks):
     out = run_emulated(ranks, lambda rt: run_stencil(rt, spec, exchange="twosided").checksum,
                        segment_bytes=_seg_bytes(nx, ny, nz, ranks))
     assert out[0] == CASES[key]["sha256"]
+
+
+def test_full_size_1024_cubed_eight_ranks_matches_reference():
+    """BASELINE configs[4] decomposition: 1024^3 on 8 emulated ranks (x-slabs of
+    128 planes, spread over the visible GPUs), 3 steps -- sha256 equal to the
+    reference's own 8-rank run."""
+    import torch
+
+    from paper_2506_02486_b200.apps.stencil import StencilSpec, run_stencil
+    from paper_2506_02486_b200.emulate import run_emulated
+    want = [c for c in GOLD.get("full_size", []) if c["nx"] == 1024 and 8 in c["ranks_reference"]]
+    if not want:
+        pytest.skip("full-size golden not recorded")
+    seg = _seg_bytes(1024, 1024, 1024, 8)
+    per_gpu = -(-8 // NGPU) * seg
+    if torch.cuda.mem_get_info(0)[0] < per_gpu + (24 << 30):
+        pytest.skip("needs the 8 segments' HBM free")
+    spec = StencilSpec(1024, 1024, 1024, steps=3)
+    out = run_emulated(8, lambda rt: run_stencil(rt, spec).checksum, segment_bytes=seg,
+                       timeout=900.0)
+    assert out[0] == want[0]["sha256"]
 
 
 def test_baseline_config1_128cubed_two_ranks():
