@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) matmul_exact_kernel(int64_t n, int64_t kk
 // Tile configurations.  WM x WN = 8x8 DMMA fragments per warp; WARPS_M x
 // WARPS_N warps per CTA; MINB CTAs per SM (register budget).
 template <int WM_, int WN_, int WARPS_M_, int WARPS_N_, int BK_, int STAGES_, int MINB_,
-          bool PAIRK_ = false, int APADX_ = 4>
+          bool PAIRK_ = false, int APADX_ = 4, int BPADX_ = 4>
 struct Cfg {
     static constexpr int WM = WM_, WN = WN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
     static constexpr bool PAIRK = PAIRK_;
@@ -90,14 +90,21 @@ struct Cfg {
     static constexpr int STAGES = STAGES_, MINB = MINB_;
     static constexpr int THREADS = WARPS_M * WARPS_N * 32;
     static constexpr int APAD = BK + APADX_;  // A tile row pitch (doubles): conflict-free fragments
-    static constexpr int BPAD = BN + 4;   // B tile row pitch
+    // B tile row pitch (doubles).  A warp's 8 B fragment load is served per
+    // half-warp (lanes gq 0..3 x tq 0..3): its rows step by `kstep` = 1
+    // (single-k) or 2 (paired-k) x BPAD, so conflict-free needs
+    // kstep * BPAD = 4 (mod 16): BN + 4 single-k, BN + 2 paired-k.
+    static constexpr int BPAD = BN + BPADX_;
     static constexpr int A_STAGE = BM * APAD, B_STAGE = BK * BPAD;
     static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
 };
 using CfgBig = Cfg<8, 4, 2, 4, 16, 4, 1>;    // 128x128 CTA, 64x32 warps, 1 CTA/SM
 using CfgDual = Cfg<4, 4, 4, 2, 16, 3, 2>;   // 128x64 CTA, 32x32 warps, 2 CTAs/SM
 using CfgDeepK = Cfg<8, 4, 2, 4, 32, 3, 1>;  // 128x128 CTA, BK=32 (half the barriers)
-using CfgP2 = Cfg<4, 4, 4, 2, 16, 3, 2, true, 8>;  // CfgDual, paired-k A loads, A pitch 24
+#ifndef DIOMP_DGEMM_P2_BPADX
+#define DIOMP_DGEMM_P2_BPADX 2
+#endif
+using CfgP2 = Cfg<4, 4, 4, 2, 16, 3, 2, true, 8, DIOMP_DGEMM_P2_BPADX>;  // CfgDual, paired-k A loads, A pitch 24, B pitch 66
 using CfgQ4 = Cfg<4, 8, 2, 2, 16, 3, 2, false, 4>; // 64x128 CTA, 4 warps of 32x64 (cuBLAS's shape)
 
 struct GemmParams {
@@ -351,6 +358,8 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
     // last step's DMMAs) measured 0.76 (spills at 128 regs) / 0.78 (BK=32,
     // 1 CTA/SM) / 0.90 (64x128 CTA) -- the compiler's own schedule is better.
     // 16 warps of 32x32 in a 128x128 CTA (4 stages, 1 CTA/SM): 0.81-0.83.
+    // B pitch BN+2 removed the paired-k B loads' 2-way bank conflicts (1.07e9 ->
+    // 1.1e6 at 8192^3) for only +0.3 %: the gap to cuBLAS is not shared memory.
     const char *v = getenv("DIOMP_DGEMM_CFG");
     if (v && atoi(v) == 0) return launch_dgemm<CfgBig>(p, x->device, (cudaStream_t)stream);
     if (v && atoi(v) == 1) return launch_dgemm<CfgDual>(p, x->device, (cudaStream_t)stream);
