@@ -414,7 +414,7 @@ def _dgemm_cli(args):
             extra["cpu_baseline"] = _cpu_dgemm_sample(n)
         _line(rt, "dgemm_ring_tflops", round(tflops, 3), "TFLOP/s", args,
               {"workload": f"cannon_ring_{n}^2_fp64", "endpoints": rt.nranks,
-               "kernel": "DMMA m8n8k4 + fused stripe shift"}, extra)
+               "kernel": "DMMA m8n8k4", "shift": ring.shift if rt.nranks > 1 else None}, extra)
     rt.finalize()
     return 0
 

@@ -6,12 +6,15 @@ stripe e; at step s it holds stripe (e+s) mod P, computes
 C_e += A_e[:, blk] @ B_held and shifts the held stripe to its predecessor.
 
 B200 execution: the product runs on the FP64 tensor cores (DMMA kernel,
-csrc/gemm.cuh) and the shift is fused into it -- every B tile the kernel
-stages in shared memory is also stored once into the predecessor's spare
-stripe over NVLink, so the transfer rides inside the GEMM instead of
-competing with it.  With every endpoint on its own GPU the ring steps are
+csrc/gemm.cuh).  With every endpoint on its own GPU the ring steps are
 ordered by device flags (wait: successor wrote my stripe, predecessor freed
-its spare; signal: both, by the last CTA).  The residual is measured against
+its spare; signal: both) and the shift runs on the copy engine from a side
+stream, concurrently with the product that reads the same stripe, so it
+costs the DMMA pipe nothing.  The alternative fused shift (every B tile the
+kernel stages in shared memory also stored into the predecessor's spare
+stripe over NVLink, DIOMP_CANNON_SHIFT=fused, and the path used when
+endpoints share a GPU) measured 5 % slower on 2 and 4 B200: the remote
+stores stall the DMMA warps (profiles/r01_cannon_shift.txt).  The residual is measured against
 the bit-exact k-ordered matmul seam (kernels.matmul_f64, the reference's
 oracle arithmetic) run on the GPU.
 """
@@ -19,6 +22,7 @@ oracle arithmetic) run on the GPU.
 from __future__ import annotations
 
 import struct
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -108,6 +112,20 @@ class CannonRing:
         torch.cuda.synchronize()
         self.sync = p > 1 and rt.distinct_gpus(self.world)
         self.step_no = 0
+        # ring shift engine with device flags: "ce" (default) = the copy engine
+        # pushes the whole stripe on a side stream while the DMMA kernel runs;
+        # "fused" = the GEMM's CTAs store each B tile from shared memory
+        # (measured 5 % slower on 2 and 4 B200: the remote stores stall the
+        # DMMA warps, profiles/r01_cannon_shift.txt)
+        self.shift = os.environ.get("DIOMP_CANNON_SHIFT", "ce") if self.sync else "fused"
+        if self.shift not in ("ce", "fused"):
+            raise ValueError(f"DIOMP_CANNON_SHIFT={self.shift!r}: expected 'ce' or 'fused'")
+        self._side = {}
+        if self.shift == "ce":
+            for _, ep in self.my_eps:
+                g = rt.gpus[ep.device]
+                self._side[ep.device] = (_native.stream_create(g), _native.event_create(g, False),
+                                         _native.event_create(g, False))
 
     def stripe(self, d: int, which: int):
         """torch view of this rank's stripe buffer `which` on device d."""
@@ -152,10 +170,31 @@ class CannonRing:
                     sync["sig_addr"].append(rt.flag_address(nb.rank, nb.device, me))
                     sync["sig_value"].append(sent + 1)
                     rt.advance_pair(me, idx, 1)
-            gemm.dgemm_raw(st["gpu"], ns, n, ns, a_blk.data_ptr(), n,
-                           rt.gm.base(d) + cur_rec.addr.offset, n, st["c"].data_ptr(), n,
+            src = rt.gm.base(d) + cur_rec.addr.offset
+            if self.shift == "ce":
+                self._ce_step(st["gpu"], d, ns, n, a_blk, src, st["c"], fwd, sync)
+                continue
+            gemm.dgemm_raw(st["gpu"], ns, n, ns, a_blk.data_ptr(), n, src, n, st["c"].data_ptr(), n,
                            self._stream(d), fwd=fwd, ldf=n, sync=sync)
         self.step_no += 1
+
+    def _ce_step(self, gpu, d, ns, n, a_blk, src, c, fwd, sync):
+        """One step with the shift on the copy engine: wait for both
+        neighbours' previous step (our stripe has arrived, the predecessor's
+        spare buffer is free) -> side stream pushes the stripe to the
+        predecessor while the DMMA kernel multiplies it -> join -> signal."""
+        main = self._stream(d)
+        side, ready, sent = self._side[d]
+        for a, v in zip(sync["wait_addr"], sync["wait_value"]):
+            _native.call("diomp_wait", gpu, a, v, main)
+        _native.call("diomp_event_record", ready, main)
+        _native.call("diomp_stream_wait_event", side, ready)
+        _native.call("diomp_put", gpu, fwd, src, self.stripe_bytes, 1, side)
+        _native.call("diomp_event_record", sent, side)
+        gemm.dgemm_raw(gpu, ns, n, ns, a_blk.data_ptr(), n, src, n, c.data_ptr(), n, main)
+        _native.call("diomp_stream_wait_event", main, sent)
+        for a, v in zip(sync["sig_addr"], sync["sig_value"]):
+            _native.call("diomp_signal", gpu, a, v, main)
 
     def synchronize(self):
         for e, ep in self.my_eps:
@@ -180,6 +219,12 @@ class CannonRing:
         self.synchronize()
 
     def release(self):
+        for side, ready, sent in self._side.values():
+            _native.call("diomp_stream_sync", side)
+            _native.call("diomp_event_destroy", ready)
+            _native.call("diomp_event_destroy", sent)
+            _native.call("diomp_stream_destroy", side)
+        self._side = {}
         if self.streams:
             for d, s in enumerate(self.streams):
                 self.rt.pools[d].release(s)

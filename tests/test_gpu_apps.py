@@ -29,27 +29,37 @@ def test_cannon_identity_exact():
     assert all(r.identity_exact for r in res)
 
 
-def test_cannon_matches_host_blas_at_1024():
-    """GPU ring product vs numpy (OpenBLAS) on the reference's own inputs."""
+@pytest.mark.parametrize("shift,ranks", [("ce", 2), ("fused", 2), ("ce", 4), ("fused", 4)])
+def test_cannon_matches_host_blas_at_1024(shift, ranks, monkeypatch):
+    """GPU ring product vs numpy (OpenBLAS) on the reference's own inputs, both
+    shift engines (copy engine on a side stream / fused into the DMMA kernel);
+    two back-to-back runs (stripes return home after P steps), so C = 2 A@B."""
     import torch
 
     from paper_2506_02486_b200.apps.cannon import CannonRing, MatmulSpec, _fill_matrices
     from paper_2506_02486_b200.emulate import run_emulated
+    monkeypatch.setenv("DIOMP_CANNON_SHIFT", shift)
     n = 1024
     a, b = _fill_matrices(n, 0)
-    want = a @ b
+    want = 2.0 * (a @ b)
 
     def fn(rt):
         ring = CannonRing(rt, MatmulSpec(n, rt.nranks), a_full=a, b_full=b)
+        mode = ring.shift
         rt.barrier(rt.world)
+        ring.run()
         ring.run()
         rt.barrier(rt.world)
         out = {e: st["c"].cpu().numpy() for e, st in ring.local.items()}
         ring.release()
-        return out
+        return out, mode
 
-    res = run_emulated(2, fn, segment_bytes=64 * MIB)
-    got = np.concatenate([res[r][r] for r in range(2)])
+    res = run_emulated(ranks, fn, segment_bytes=64 * MIB)
+    if NGPU >= ranks:
+        assert all(m == shift for _, m in res)
+    ns = n // ranks
+    got = np.concatenate([res[r][0][r] for r in range(ranks)])
+    assert got.shape == (n, n) and ns * ranks == n
     rel = np.linalg.norm(got - want) / np.linalg.norm(want)
     assert rel <= 1e-14, rel
 
