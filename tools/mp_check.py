@@ -2,7 +2,7 @@
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/mp_check.py
 Checks against the reference-generated golden fixtures: fused stencil
 checksums (device-flag halo), allreduce/reduce/bcast bitwise, put/get
-byte-exact.  Prints one JSON line per rank-0 check; exit 1 on any failure.
+byte-exact, Cannon ring (both shift engines) vs host BLAS.  Prints one JSON line per rank-0 check; exit 1 on any failure.
 """
 
 import json
@@ -91,6 +91,36 @@ def main():
                 good &= bytes(back) == data
         print(json.dumps({"check": "put_get", "ranks": k, "ok": good}), flush=True)
     ok &= good
+    rt.barrier(rt.world)
+
+    # Cannon ring over IPC-mapped stripes (copy-engine and fused shift), two
+    # back-to-back runs: each rank's C stripe vs host BLAS, 2 A@B
+    import pickle
+
+    from paper_2506_02486_b200.apps.cannon import CannonRing, MatmulSpec, _fill_matrices
+    n = 1024
+    a, b = _fill_matrices(n, 0)
+    ns = n // rt.nranks
+    want = 2.0 * (a[rt.rank * ns:(rt.rank + 1) * ns] @ b)
+    for shift in ("ce", "fused"):
+        os.environ["DIOMP_CANNON_SHIFT"] = shift
+        ring = CannonRing(rt, MatmulSpec(n, rt.nranks), a_full=a, b_full=b)
+        rt.barrier(rt.world)
+        ring.run()
+        ring.run()
+        rt.barrier(rt.world)
+        got = ring.local[rt.rank]["c"].cpu().numpy()
+        rel = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+        mode = ring.shift
+        ring.release()
+        res = [pickle.loads(x) for _, x in rt.ctrl.allgather(tuple(range(rt.nranks)), f"mpc/{shift}",
+                                                              pickle.dumps((rel, mode)))]
+        good = all(r <= 1e-14 for r, _ in res)
+        ok &= good
+        if rt.rank == 0:
+            print(json.dumps({"check": "cannon", "n": n, "ranks": rt.nranks, "shift": [m for _, m in res],
+                              "max_rel": max(r for r, _ in res), "ok": good}), flush=True)
+    os.environ.pop("DIOMP_CANNON_SHIFT", None)
     rt.barrier(rt.world)
     d.finalize(rt)
     return 0 if ok else 1
