@@ -304,3 +304,40 @@ def test_allreduce_nvls_in_switch(monkeypatch):
                 err = np.linalg.norm(nv.astype(np.float64) - w64) / max(np.linalg.norm(w64), 1e-300)
                 assert err <= tol, (et, kind, err)
     _ = torch
+
+
+@need_gpus(2)
+def test_absent_peer_surfaces_transport_failure_at_the_deadline():
+    """Peer-failure analogue of the reference's test_transport.py:221-259 and
+    its per-wait deadlines (config.py:20, 120): rank 1 never enters the
+    collective, so rank 0's device-side entry wait gives up at its deadline
+    and the call raises TransportFailure instead of hanging the GPU."""
+    import time
+
+    from paper_2506_02486_b200 import _native, errors
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200.emulate import run_emulated
+    op = coll.ReduceOp(coll.ReduceKind.Sum, coll.ElementType.f32)
+    count = 1024
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        buf = rt.alloc_symmetric(count * 4, 0)
+        out = None
+        if rt.rank == 0:
+            assert comm.device_sync
+            _native.call("diomp_set_wait_timeout", rt.gpus[0], 0.5)
+            t0 = time.perf_counter()
+            try:
+                coll.allreduce(comm, buf.addr, buf.addr, count, op)
+                out = ("no error", 0.0)
+            except errors.TransportFailure:
+                out = ("TransportFailure", time.perf_counter() - t0)
+            finally:
+                _native.call("diomp_set_wait_timeout", rt.gpus[0], float(rt.cfg.timeout))
+        rt.barrier(rt.world)   # rank 1's segment stays mapped until rank 0 is done
+        return out
+
+    res = run_emulated(2, fn, segment_bytes=64 * MIB, timeout=30.0)
+    assert res[0][0] == "TransportFailure", res[0]
+    assert 0.4 < res[0][1] < 10.0, res[0]
