@@ -168,6 +168,11 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
  * flags, measured slower on B200); otherwise every non-root pulls its 1/(k-1)
  * block from the root and pushes it to the other non-roots.  Same bytes.    */
 int diomp_set_bcast_chain_min(uint64_t bytes);
+/* chain flavour for the sizes above: on = pull chain (every hop loads its chunk
+ * from its predecessor over NVLink and stores it locally, so the per-chunk
+ * fence drains local writes only), off = push chain (default;
+ * DIOMP_BCAST_ALGO=pullchain sets on).                                       */
+int diomp_set_bcast_pullchain(int32_t on);
 int diomp_reduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
                  int32_t dtype, int32_t op, int32_t root, void *stream);
 int diomp_set_allreduce_ce_min(uint64_t bytes);

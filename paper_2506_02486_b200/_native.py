@@ -109,6 +109,7 @@ _PROTOS = {
     "diomp_team_barrier": [ctypes.POINTER(Team), c_vp],
     "diomp_bcast": [ctypes.POINTER(Team), c_u64, c_u64, c_i32, c_vp],
     "diomp_set_bcast_chain_min": [c_u64],
+    "diomp_set_bcast_pullchain": [c_i32],
     "diomp_reduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_i32, c_vp],
     "diomp_set_allreduce_ce_min": [c_u64],
     "diomp_mc_supported": [ctypes.c_int, ctypes.POINTER(ctypes.c_int)],

@@ -370,8 +370,71 @@ __global__ void __launch_bounds__(THREADS) bcast_chain_kernel(const __grid_const
     exit_barrier(a.t);
 }
 
+// bcast, pull chain: the same root -> root+1 -> ... pipeline, but every hop
+// LOADS its chunk from its predecessor's buffer over NVLink and stores it to
+// its own HBM.  All the hop's stores are local, so the system fence before
+// each progress flag drains local writes only instead of NVLink write acks
+// (what made the push chain fence-bound), and every link carries the buffer
+// once as read responses -- the "readers" pattern of tools/fanout_probe.cu,
+// the fastest one measured (765 GB/s at 1 GiB on 4 B200).  The root does no
+// data work.  Flags as the push chain: the predecessor's CTA b publishes
+// (E << 32) | chunks into this position's scratch after its local stores.
+__global__ void __launch_bounds__(THREADS) bcast_pullchain_kernel(const __grid_constant__ Args a,
+                                                                  uint64_t chv) {
+    entry_barrier(a.t);
+    const diomp_team &t = a.t;
+    const int k = t.k, p = t.pos, root = a.root;
+    const int h = (p - root + k) % k;
+    const int succ = (p + 1) % k, pred = (p + k - 1) % k;
+    const uint64_t off = a.send_off, n = a.count;
+    const uint64_t al = (off + 15) & ~(uint64_t)15;
+    const uint64_t body_lo = al - off < n ? al - off : n;
+    const uint64_t nvec = (n - body_lo) / 16, body_hi = body_lo + nvec * 16;
+    const uint4 *from = reinterpret_cast<const uint4 *>(t.base[pred] + off + body_lo);
+    uint4 *mine = reinterpret_cast<uint4 *>(t.base[p] + off + body_lo);
+    const uint64_t E = (uint64_t)(t.epoch_from[pred] + 1) << 32;
+    const uint64_t Eo = (uint64_t)(t.epoch_to[succ] + 1) << 32;
+    const uint64_t nch = (nvec + chv - 1) / chv;
+    uint64_t i = 0;
+    for (uint64_t c = blockIdx.x; h > 0 && c < nch; c += gridDim.x, ++i) {
+        if (h > 1) {   // the root's buffer is complete at entry
+            if (threadIdx.x == 0) wait_ge(chain_flag(t, p, pred, blockIdx.x), E | (i + 1));
+            __syncthreads();
+        }
+        const uint64_t lo = c * chv, hi = lo + chv < nvec ? lo + chv : nvec;
+        uint64_t v = lo + threadIdx.x;
+        for (; v + (CHAIN_U - 1) * THREADS < hi; v += CHAIN_U * THREADS) {
+            uint4 r[CHAIN_U];
+#pragma unroll
+            for (int u = 0; u < CHAIN_U; ++u) r[u] = __ldcg(from + v + u * THREADS);
+#pragma unroll
+            for (int u = 0; u < CHAIN_U; ++u) mine[v + u * THREADS] = r[u];
+        }
+        for (; v < hi; v += THREADS) mine[v] = __ldcg(from + v);
+        if (h < k - 1) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence_system();
+                st_release_sys(chain_flag(t, succ, p, blockIdx.x), Eo | (i + 1));
+            }
+        }
+    }
+    if (h == 0 && blockIdx.x == 0) {
+        const uint8_t *s8 = reinterpret_cast<const uint8_t *>(t.base[root] + off);
+        const uint64_t ntail = n - body_hi;
+        for (uint64_t e0 = threadIdx.x; e0 < body_lo + ntail; e0 += THREADS) {
+            const uint64_t e = e0 < body_lo ? e0 : body_hi + (e0 - body_lo);
+            const uint8_t b = s8[e];
+            for (int q = 0; q < k; ++q)
+                if (q != root) reinterpret_cast<uint8_t *>(t.base[q] + off)[e] = b;
+        }
+    }
+    exit_barrier(a.t);
+}
+
 // bcast algorithm: chain for k >= 3 from DIOMP_BCAST_CHAIN_MIN bytes (default
-// never, see above), else pull+push.  DIOMP_BCAST_ALGO=pull|chain forces one.
+// never, see above), else pull+push.  DIOMP_BCAST_ALGO=pull|chain forces one;
+// DIOMP_BCAST_ALGO=pullchain selects the pull chain for the chain sizes.
 static std::atomic<uint64_t> g_bcast_chain_min{~0ull};
 static std::once_flag g_bc_once;
 
@@ -381,9 +444,24 @@ static uint64_t bcast_chain_min() {
         const char *e = getenv("DIOMP_BCAST_CHAIN_MIN");
         if (e) g_bcast_chain_min = (uint64_t)strtoull(e, nullptr, 10);
         if (algo && !strcmp(algo, "pull")) g_bcast_chain_min = ~0ull;
-        if (algo && !strcmp(algo, "chain")) g_bcast_chain_min = 0;
+        if (algo && (!strcmp(algo, "chain") || !strcmp(algo, "pullchain"))) g_bcast_chain_min = 0;
     });
     return g_bcast_chain_min.load(std::memory_order_relaxed);
+}
+
+// chain flavour: 1 = pull chain, 0 = push chain (DIOMP_BCAST_ALGO=pullchain
+// or diomp_set_bcast_pullchain).
+static std::atomic<int> g_bcast_pullchain{-1};
+
+static bool bcast_pullchain() {
+    int v = g_bcast_pullchain.load(std::memory_order_relaxed);
+    if (v < 0) {
+        const char *e = getenv("DIOMP_BCAST_ALGO");
+        int want = (e && !strcmp(e, "pullchain")) ? 1 : 0;
+        g_bcast_pullchain.compare_exchange_strong(v, want);
+        v = g_bcast_pullchain.load(std::memory_order_relaxed);
+    }
+    return v == 1;
 }
 
 // CTAs per SM (512 threads each).  Measured through the C ABI
@@ -502,6 +580,11 @@ int diomp_set_bcast_chain_min(uint64_t bytes) {
     return DIOMP_OK;
 }
 
+int diomp_set_bcast_pullchain(int32_t on) {
+    diomp::coll::g_bcast_pullchain.store(on ? 1 : 0, std::memory_order_relaxed);
+    return DIOMP_OK;
+}
+
 int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
                     int32_t dtype, int32_t op, void *stream) {
     using namespace diomp::coll;
@@ -560,7 +643,8 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
         const uint64_t chv = std::max<uint64_t>(env_chunk / 16, 32);
         const uint64_t nch = (nvec + chv - 1) / chv;
         const int g = (int)std::min<uint64_t>((uint64_t)env_g, nch);
-        bcast_chain_kernel<<<g, THREADS, 0, (cudaStream_t)stream>>>(a, chv);
+        if (bcast_pullchain()) bcast_pullchain_kernel<<<g, THREADS, 0, (cudaStream_t)stream>>>(a, chv);
+        else bcast_chain_kernel<<<g, THREADS, 0, (cudaStream_t)stream>>>(a, chv);
         DIOMP_LAUNCH_CHECK();
         return DIOMP_OK;
     }

@@ -147,8 +147,10 @@ def test_device_flag_mode_back_to_back():
 
 
 @need_gpus(3)
-def test_bcast_chain_device_flags():
-    """Chain bcast (k >= 3, per-CTA progress flags): every member ends with
+@pytest.mark.parametrize("pull", [0, 1])
+def test_bcast_chain_device_flags(pull):
+    """Chain bcast (k >= 3, per-CTA progress flags), push and pull flavours:
+    every member ends with
     the root's bytes -- odd sizes and offsets, every root, repeated, mixed with
     pull+push bcasts and allreduces so the progress-flag values must stay
     monotone across calls and algorithms."""
@@ -179,10 +181,12 @@ def test_bcast_chain_device_flags():
             coll.allreduce(comm, acc.addr, acc.addr, 1000, op)
         return out
 
+    _native.call("diomp_set_bcast_pullchain", pull)
     try:
         res = run_emulated(k, fn, segment_bytes=128 * MIB)
     finally:
         _native.call("diomp_set_bcast_chain_min", (1 << 64) - 1)
+        _native.call("diomp_set_bcast_pullchain", 0)
     for i in range(len(plan)):
         snap = next(r[i][0] for r in res if r[i][0] is not None)
         assert all(r[i][1] == snap for r in res), i
