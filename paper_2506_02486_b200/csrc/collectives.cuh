@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(THREADS) reduce_kernel(const __grid_constant__
 __global__ void allreduce_exit_kernel(const __grid_constant__ Args a) { exit_barrier(a.t, 3); }
 
 // bcast: non-root position p handles block j = (p - root - 1 mod k) of k-1.
+template <int U>
 __global__ void __launch_bounds__(THREADS) bcast_kernel(const __grid_constant__ Args a) {
     entry_barrier(a.t);
     const diomp_team &t = a.t;
@@ -253,7 +254,6 @@ __global__ void __launch_bounds__(THREADS) bcast_kernel(const __grid_constant__ 
         const uint4 *src = reinterpret_cast<const uint4 *>(t.base[root] + off + body_lo);
         const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
         const uint64_t gsz = (uint64_t)gridDim.x * blockDim.x;
-        constexpr int U = 4;
         uint64_t v = vlo + gtid;
         for (; v + (U - 1) * gsz < vhi; v += U * gsz) {
             uint4 b[U];
@@ -650,7 +650,19 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
     }
     const uint64_t per = nbytes / (uint64_t)(team->k - 1) / 16 + 1;
     const int g = grid_for(per, ctas_per_sm(nbytes, false));
-    bcast_kernel<<<g, THREADS, 0, (cudaStream_t)stream>>>(a);
+    // 16-B vectors in flight per thread (DIOMP_BCAST_U = 2 | 4 | 8 overrides).
+    // Measured on 4 B200 (profiles/r01_bcast_u_sweep.txt): 2 beats 4 and 8 at
+    // 2 CTAs/SM from 32 MiB -- fewer outstanding NVLink loads per SM, less
+    // congestion (k=4: 64 MiB 575 vs 518 GB/s, 1 GiB 608 vs 599; k=3/k=2 also
+    // ahead); only k=4 below 32 MiB keeps 4 (16 MiB: 402 vs 390).
+    static const int env_u = [] {
+        const char *e = getenv("DIOMP_BCAST_U");
+        return e ? atoi(e) : 0;
+    }();
+    const int u = env_u ? env_u : (team->k >= 4 && nbytes < (32ull << 20) ? 4 : 2);
+    if (u == 4) bcast_kernel<4><<<g, THREADS, 0, (cudaStream_t)stream>>>(a);
+    else if (u == 8) bcast_kernel<8><<<g, THREADS, 0, (cudaStream_t)stream>>>(a);
+    else bcast_kernel<2><<<g, THREADS, 0, (cudaStream_t)stream>>>(a);
     DIOMP_LAUNCH_CHECK();
     return DIOMP_OK;
 }
