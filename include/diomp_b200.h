@@ -249,8 +249,15 @@ typedef struct {
     uint64_t to_left, to_right;         /* signals already sent per neighbour             */
     uint64_t counter;                   /* u32 in own segment (last-CTA detection)        */
 } diomp_stencil_plan;
-/* Launch steps [step0, step0+nsteps) on `stream`; each step signals both
- * neighbours once (caller advances the from/to counters by nsteps).        */
+/* Launch steps [step0, step0+nsteps) on `stream`.  With sync, every call
+ * raises nsteps + 1 signals per neighbour (an entry signal, then one per
+ * finished step) and waits for as many; the caller advances the from/to
+ * counters by nsteps + 1.  The entry handshake means no halo store of this
+ * call can land in a neighbour's ghost planes before the neighbour's stream
+ * reached the call (its field initialisation / H2D copies are complete).
+ * sync = 0 with neighbour fields set is the host-ordered fused mode (one
+ * step per call, host barrier between calls); it needs the TMA fast path
+ * (R = 4, even NZ, 16 B aligned) and returns DIOMP_BAD_REQUEST otherwise. */
 int diomp_stencil_run(const diomp_stencil_plan *plan, int64_t step0, int64_t nsteps,
                       void *stream);
 

@@ -13,6 +13,10 @@ B200 execution (StencilRunner):
     with no host involvement;
   * listing1 (ranks sharing a GPU): the reference's order -- exchange()
     puts + fence + barrier, then the update kernel -- host-synchronised;
+  * fused_host: the fused kernel (halo stores from its epilogue straight
+    into the neighbours' ghost planes) ordered by a host barrier per step
+    instead of device flags -- valid for ranks sharing a GPU, and the way a
+    one-GPU box exercises the fused epilogue's peer stores;
   * twosided (exchange="twosided"): the reference's mailbox send/recv
     comparison variant (apps/halo_twosided.py), host-synchronised.
 """
@@ -106,7 +110,7 @@ class StencilRunner:
 
         if mode is None:
             mode = "fused" if (nranks == 1 or rt.distinct_gpus(rt.world.members)) else "listing1"
-        if mode not in ("fused", "listing1", "twosided"):
+        if mode not in ("fused", "fused_host", "listing1", "twosided"):
             raise UsageError(f"unknown stencil mode {mode!r}")
         self.mode = mode
         self.mailbox = None
@@ -129,7 +133,7 @@ class StencilRunner:
         p.NX, p.NY, p.NZ = self.shape
         offs = (self.field_a.addr.offset, self.field_b.addr.offset)
         p.field[0], p.field[1] = (rt.gm.base(0) + o for o in offs)
-        fused = self.mode == "fused"
+        fused = self.mode in ("fused", "fused_host")
         if fused and self.left is not None:
             p.left_field[0], p.left_field[1] = (rt.peer_address(self.left, 0, o) for o in offs)
         if fused and self.right is not None:
@@ -139,7 +143,7 @@ class StencilRunner:
         p.center = float(self.center)
         for t in range(r + 1):
             p.w[t] = float(self.w[t])
-        p.sync = 1 if (fused and rt.nranks > 1) else 0
+        p.sync = 1 if (self.mode == "fused" and rt.nranks > 1) else 0
         if p.sync:
             for side, nb in (("left", self.left), ("right", self.right)):
                 if nb is None:
@@ -163,7 +167,8 @@ class StencilRunner:
         if plan.sync:
             for nb in (self.left, self.right):
                 if nb is not None:
-                    self.rt.advance_pair(self.me_idx, self.rt.endpoint_index(nb, 0), nsteps)
+                    # nsteps + 1 signals per call: entry + one per step
+                    self.rt.advance_pair(self.me_idx, self.rt.endpoint_index(nb, 0), nsteps + 1)
         self.step += nsteps
 
     def run(self, nsteps: int):
@@ -173,6 +178,21 @@ class StencilRunner:
             self.enqueue(nsteps)
             self.stream.synchronize()
             _native.check_device(self.gpu, "stencil")
+            return
+        if self.mode == "fused_host":
+            # step s writes the neighbours' ghost planes of field[s%2], which
+            # they last read (as u_cur) in step s-1: a barrier after every
+            # rank's step s-1 has drained orders the two
+            for _ in range(nsteps):
+                if rt.nranks > 1:
+                    rt.barrier(rt.world)
+                _native.check(_native.lib.diomp_stencil_run(self._plan(), self.step, 1,
+                                                            self.stream.handle), "stencil_run")
+                self.stream.synchronize()
+                _native.check_device(self.gpu, "stencil")
+                self.step += 1
+            if rt.nranks > 1:
+                rt.barrier(rt.world)
             return
         for _ in range(nsteps):
             cur = self.field_b if self.step % 2 == 0 else self.field_a

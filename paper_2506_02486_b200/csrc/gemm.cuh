@@ -128,6 +128,12 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pr
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pred) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    const int n = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(n)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -140,33 +146,39 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-template <class C>
+template <class C, bool VEC>
 __device__ __forceinline__ void load_tiles(const GemmParams &p, double *As, double *Bs, int64_t m0,
                                            int64_t n0, int64_t k0) {
-    // A: BM x BK in 16 B chunks; B: BK x BN in 16 B chunks (trip counts are
-    // compile-time so the loops unroll)
-    constexpr int NA = C::BM * C::BK / 2, NB = C::BK * C::BN / 2;
+    // A: BM x BK, B: BK x BN, in 16 B chunks (VEC: even K/N/ld, 16 B aligned
+    // bases) or single doubles (any shape); trip counts are compile-time so
+    // the loops unroll
+    constexpr int W = VEC ? 2 : 1;
+    constexpr int NA = C::BM * C::BK / W, NB = C::BK * C::BN / W;
 #pragma unroll
     for (int it = 0; it < (NA + C::THREADS - 1) / C::THREADS; ++it) {
         const int e = threadIdx.x + it * C::THREADS;
         if (NA % C::THREADS && e >= NA) break;
-        const int r = e / (C::BK / 2), ch = e % (C::BK / 2);
-        const int64_t gr = m0 + r, gk = k0 + ch * 2;
+        const int r = e / (C::BK / W), ch = e % (C::BK / W);
+        const int64_t gr = m0 + r, gk = k0 + ch * W;
         const bool ok = gr < p.M && gk < p.K;
-        cp_async16(As + r * C::APAD + ch * 2, ok ? (const void *)(p.A + gr * p.lda + gk) : (const void *)p.A, ok);
+        const void *g = ok ? (const void *)(p.A + gr * p.lda + gk) : (const void *)p.A;
+        if (VEC) cp_async16(As + r * C::APAD + ch * W, g, ok);
+        else cp_async8(As + r * C::APAD + ch * W, g, ok);
     }
 #pragma unroll
     for (int it = 0; it < (NB + C::THREADS - 1) / C::THREADS; ++it) {
         const int e = threadIdx.x + it * C::THREADS;
         if (NB % C::THREADS && e >= NB) break;
-        const int r = e / (C::BN / 2), ch = e % (C::BN / 2);
-        const int64_t gk = k0 + r, gn = n0 + ch * 2;
+        const int r = e / (C::BN / W), ch = e % (C::BN / W);
+        const int64_t gk = k0 + r, gn = n0 + ch * W;
         const bool ok = gk < p.K && gn < p.N;
-        cp_async16(Bs + r * C::BPAD + ch * 2, ok ? (const void *)(p.B + gk * p.ldb + gn) : (const void *)p.B, ok);
+        const void *g = ok ? (const void *)(p.B + gk * p.ldb + gn) : (const void *)p.B;
+        if (VEC) cp_async16(Bs + r * C::BPAD + ch * W, g, ok);
+        else cp_async8(Bs + r * C::BPAD + ch * W, g, ok);
     }
 }
 
-template <class C>
+template <class C, bool VEC>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_dmma_kernel(const __grid_constant__ GemmParams p) {
     extern __shared__ __align__(16) double gsm[];
     double *As = gsm;
@@ -203,7 +215,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_dmma_kernel(const _
     const int64_t ktiles = ceil_div(p.K, C::BK);
 #pragma unroll
     for (int s = 0; s < C::STAGES - 1; ++s) {
-        if (s < ktiles) load_tiles<C>(p, As + s * C::A_STAGE, Bs + s * C::B_STAGE, m0, n0, (int64_t)s * C::BK);
+        if (s < ktiles) load_tiles<C, VEC>(p, As + s * C::A_STAGE, Bs + s * C::B_STAGE, m0, n0, (int64_t)s * C::BK);
         cp_async_commit();
     }
     for (int64_t kt = 0; kt < ktiles; ++kt) {
@@ -216,7 +228,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_dmma_kernel(const _
         const int64_t nk = kt + C::STAGES - 1;
         if (nk < ktiles) {
             const int ns = (int)(nk % C::STAGES);
-            load_tiles<C>(p, As + ns * C::A_STAGE, Bs + ns * C::B_STAGE, m0, n0, nk * C::BK);
+            load_tiles<C, VEC>(p, As + ns * C::A_STAGE, Bs + ns * C::B_STAGE, m0, n0, nk * C::BK);
         }
         cp_async_commit();
         // fused ring shift: forward this B tile once to the predecessor
@@ -224,9 +236,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_dmma_kernel(const _
             for (int e = threadIdx.x; e < C::BK * C::BN / 2; e += C::THREADS) {
                 const int r = e / (C::BN / 2), ch = e % (C::BN / 2);
                 const int64_t gk = kt * C::BK + r, gn = n0 + ch * 2;
-                if (gk < p.K && gn < p.N)
-                    *reinterpret_cast<double2 *>(p.fwd + gk * p.ldf + gn) =
-                        *reinterpret_cast<const double2 *>(b_s + r * C::BPAD + ch * 2);
+                if (gk < p.K && gn < p.N) {
+                    if (VEC) {
+                        *reinterpret_cast<double2 *>(p.fwd + gk * p.ldf + gn) =
+                            *reinterpret_cast<const double2 *>(b_s + r * C::BPAD + ch * 2);
+                    } else {
+                        p.fwd[gk * p.ldf + gn] = b_s[r * C::BPAD + ch * 2];
+                        if (gn + 1 < p.N) p.fwd[gk * p.ldf + gn + 1] = b_s[r * C::BPAD + ch * 2 + 1];
+                    }
+                }
             }
         }
         if (C::PAIRK) {
@@ -279,7 +297,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_dmma_kernel(const _
         for (int j = 0; j < C::WN; ++j) {
             const int64_t r = m0 + wm + i * 8 + gq;
             const int64_t cidx = n0 + wn + j * 8 + tq * 2;
-            if (r < p.M && cidx + 1 < p.N) {
+            if (VEC && r < p.M && cidx + 1 < p.N) {
                 double2 *cp = reinterpret_cast<double2 *>(p.C + r * p.ldc + cidx);
                 double2 cv = *cp;
                 cv.x = __dadd_rn(cv.x, acc[i][j][0]);
@@ -287,6 +305,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_dmma_kernel(const _
                 *cp = cv;
             } else if (r < p.M && cidx < p.N) {
                 p.C[r * p.ldc + cidx] = __dadd_rn(p.C[r * p.ldc + cidx], acc[i][j][0]);
+                if (!VEC && cidx + 1 < p.N)
+                    p.C[r * p.ldc + cidx + 1] = __dadd_rn(p.C[r * p.ldc + cidx + 1], acc[i][j][1]);
             }
         }
 
@@ -294,16 +314,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_dmma_kernel(const _
         st_release_sys(p.sig_addr[threadIdx.x], p.sig_value[threadIdx.x]);
 }
 
-template <class C>
+template <class C, bool VEC = true>
 static int launch_dgemm(const GemmParams &p, int device, cudaStream_t s) {
     static bool attr_set[64] = {false};
     if (device < 64 && !attr_set[device]) {
-        DIOMP_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        DIOMP_CUDA_TRY(cudaFuncSetAttribute(dgemm_dmma_kernel<C, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)C::SMEM));
         attr_set[device] = true;
     }
     const int64_t tiles = ceil_div(p.M, C::BM) * ceil_div(p.N, C::BN);
-    dgemm_dmma_kernel<C><<<(unsigned)tiles, C::THREADS, C::SMEM, s>>>(p);
+    dgemm_dmma_kernel<C, VEC><<<(unsigned)tiles, C::THREADS, C::SMEM, s>>>(p);
     DIOMP_LAUNCH_CHECK();
     return DIOMP_OK;
 }
@@ -330,10 +350,14 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
     using namespace diomp;
     using namespace diomp::gemm;
     if (x->M <= 0 || x->N <= 0) return DIOMP_OK;
-    // 16 B cp.async needs even leading dimensions / K / N and aligned bases
-    if ((x->K & 1) || (x->N & 1) || (x->lda & 1) || (x->ldb & 1) || (x->ldc & 1) ||
-        ((x->A | x->B | x->C | x->fwd) & 15) || (x->fwd && (x->ldf & 1)))
+    if (x->K < 0 || x->lda < x->K || x->ldb < x->N || x->ldc < x->N || (x->fwd && x->ldf < x->N) ||
+        ((x->A | x->B | x->C | x->fwd) & 7))
         return DIOMP_BAD_REQUEST;
+    // 16 B cp.async needs even leading dimensions / K / N and 16 B aligned
+    // bases; any other shape (e.g. an odd ring stripe width n/P) takes the
+    // same kernel with 8 B operand copies and scalar epilogue stores
+    const bool vec = !((x->K & 1) || (x->N & 1) || (x->lda & 1) || (x->ldb & 1) || (x->ldc & 1) ||
+                       ((x->A | x->B | x->C | x->fwd) & 15) || (x->fwd && (x->ldf & 1)));
     DIOMP_CUDA_TRY(cudaSetDevice(x->device));
     GemmParams p{};
     p.M = x->M; p.N = x->N; p.K = x->K;
@@ -360,6 +384,7 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
     // 16 warps of 32x32 in a 128x128 CTA (4 stages, 1 CTA/SM): 0.81-0.83.
     // B pitch BN+2 removed the paired-k B loads' 2-way bank conflicts (1.07e9 ->
     // 1.1e6 at 8192^3) for only +0.3 %: the gap to cuBLAS is not shared memory.
+    if (!vec) return launch_dgemm<CfgP2, false>(p, x->device, (cudaStream_t)stream);
     const char *v = getenv("DIOMP_DGEMM_CFG");
     if (v && atoi(v) == 0) return launch_dgemm<CfgBig>(p, x->device, (cudaStream_t)stream);
     if (v && atoi(v) == 1) return launch_dgemm<CfgDual>(p, x->device, (cudaStream_t)stream);

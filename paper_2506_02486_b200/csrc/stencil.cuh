@@ -646,7 +646,30 @@ int diomp_stencil_run(const diomp_stencil_plan *pl, int64_t step0, int64_t nstep
                    make_plane_map(&pmaps[b], (const double *)pl->field[b], pl->NX, pl->NY, pl->NZ, false) == DIOMP_OK;
     }
     const int64_t plane = pl->NY * pl->NZ;
+    const bool nbrs = (pl->left_field[0] | pl->left_field[1] | pl->right_field[0] | pl->right_field[1]) != 0;
+    // the generic path stores halos before its update: without device flags
+    // nothing would order those stores after the neighbour's reads
+    if (!fast && nbrs && !pl->sync) return DIOMP_BAD_REQUEST;
     static const int edge_first = getenv("DIOMP_STENCIL_EDGE_FIRST") ? atoi(getenv("DIOMP_STENCIL_EDGE_FIRST")) : 0;
+    // Device flags per neighbour pair, nsteps + 1 signals per call:
+    //   +1        entry: this call's first kernel started, so everything the
+    //             caller enqueued before it on this stream (field init, H2D
+    //             copies, the previous call) is complete
+    //   +1+k+1    step step0+k finished (k = 0 .. nsteps-1)
+    // Step k stores into a neighbour's ghost planes only once the neighbour
+    // reported +1+k (entered, and finished its step step0+k-1, the last
+    // reader of those planes).
+    if (!fast && pl->sync && nbrs) {
+        if (pl->left_field[0]) {
+            signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_left, pl->to_left + 1);
+            wait_kernel<<<1, 1, 0, s>>>((const uint64_t *)pl->wait_left, pl->from_left + 1);
+        }
+        if (pl->right_field[0]) {
+            signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_right, pl->to_right + 1);
+            wait_kernel<<<1, 1, 0, s>>>((const uint64_t *)pl->wait_right, pl->from_right + 1);
+        }
+        DIOMP_LAUNCH_CHECK();
+    }
     for (int64_t st = step0; st < step0 + nsteps; ++st) {
         const int pb = (int)(st & 1), cb = 1 - pb;  // prev = field[s%2], cur = field[(s+1)%2]
         const int64_t k = st - step0;
@@ -667,16 +690,13 @@ int diomp_stencil_run(const diomp_stencil_plan *pl, int64_t step0, int64_t nstep
             if (p.sync) {
                 p.wait_l = pl->left_field[pb] ? (const uint64_t *)pl->wait_left : nullptr;
                 p.wait_r = pl->right_field[pb] ? (const uint64_t *)pl->wait_right : nullptr;
-                p.wl = pl->from_left + k;     // left finished step st-1
-                p.wr = pl->from_right + k;
-                // completion of step st-1 (the first step of this call has
-                // nothing to announce: the previous call's trailing signal did)
-                if (k > 0) {
-                    p.sig_l = pl->left_field[pb] ? (uint64_t *)pl->sig_left : nullptr;
-                    p.sig_r = pl->right_field[pb] ? (uint64_t *)pl->sig_right : nullptr;
-                }
-                p.sl = pl->to_left + k;
-                p.sr = pl->to_right + k;
+                p.wl = pl->from_left + 1 + k;   // left entered / finished step st-1
+                p.wr = pl->from_right + 1 + k;
+                // block 0 announces entry (k = 0) or step st-1's completion
+                p.sig_l = pl->left_field[pb] ? (uint64_t *)pl->sig_left : nullptr;
+                p.sig_r = pl->right_field[pb] ? (uint64_t *)pl->sig_right : nullptr;
+                p.sl = pl->to_left + 1 + k;
+                p.sr = pl->to_right + 1 + k;
                 p.counter = (unsigned int *)pl->counter;
             }
             int rc = launch_fast(maps[cb], pmaps[pb], p, s);
@@ -684,9 +704,9 @@ int diomp_stencil_run(const diomp_stencil_plan *pl, int64_t step0, int64_t nstep
             if (p.sync && st == step0 + nsteps - 1) {
                 // the last step's completion: a one-thread kernel behind it
                 if (pl->left_field[pb])
-                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_left, pl->to_left + k + 1);
+                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_left, pl->to_left + k + 2);
                 if (pl->right_field[pb])
-                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_right, pl->to_right + k + 1);
+                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_right, pl->to_right + k + 2);
                 DIOMP_LAUNCH_CHECK();
             }
         } else {
@@ -704,12 +724,12 @@ int diomp_stencil_run(const diomp_stencil_plan *pl, int64_t step0, int64_t nstep
             }
             if (pl->sync) {
                 if (pl->left_field[cb]) {
-                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_left, pl->to_left + k + 1);
-                    wait_kernel<<<1, 1, 0, s>>>((const uint64_t *)pl->wait_left, pl->from_left + k + 1);
+                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_left, pl->to_left + k + 2);
+                    wait_kernel<<<1, 1, 0, s>>>((const uint64_t *)pl->wait_left, pl->from_left + k + 2);
                 }
                 if (pl->right_field[cb]) {
-                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_right, pl->to_right + k + 1);
-                    wait_kernel<<<1, 1, 0, s>>>((const uint64_t *)pl->wait_right, pl->from_right + k + 1);
+                    signal_kernel<<<1, 1, 0, s>>>((uint64_t *)pl->sig_right, pl->to_right + k + 2);
+                    wait_kernel<<<1, 1, 0, s>>>((const uint64_t *)pl->wait_right, pl->from_right + k + 2);
                 }
                 DIOMP_LAUNCH_CHECK();
             }

@@ -11,7 +11,8 @@ pytestmark = pytest.mark.gpu
 MIB = 1 << 20
 
 
-@pytest.mark.parametrize("n,p", [(48, 1), (48, 2), (256, 2), (96, 3), (512, 4)])
+@pytest.mark.parametrize("n,p", [(48, 1), (48, 2), (256, 2), (96, 3), (512, 4),
+                                 (25, 1), (90, 2), (75, 3), (132, 4)])
 def test_cannon_residual(n, p):
     from paper_2506_02486_b200.apps.cannon import MatmulSpec, cannon_matmul
     from paper_2506_02486_b200.emulate import run_emulated

@@ -19,9 +19,14 @@ def _ranks_gpus():
     return [0, 1] if NGPU >= 2 else [0]
 
 
-def test_put_get_1gib_byte_exact():
+@pytest.mark.parametrize("force_remote", [False, True])
+def test_put_get_1gib_byte_exact(force_remote, monkeypatch):
+    """force_remote: DIOMP_FORCE_REMOTE=1 makes a one-GPU box take the remote
+    engines too (copy-engine put, bulk-TMA get) -- the paths a peer GPU uses."""
     import paper_2506_02486_b200 as d
     from paper_2506_02486_b200.emulate import run_emulated
+    if force_remote:
+        monkeypatch.setenv("DIOMP_FORCE_REMOTE", "1")
     payload = np.random.default_rng(2024).integers(0, 256, GIB, dtype=np.uint8)
 
     def fn(rt):

@@ -37,7 +37,8 @@ def test_matmul_seam_vs_oracle_odd_shape():
     assert np.array_equal(c.cpu().numpy().view(np.uint64), O.matmul_f64(a, b).view(np.uint64))
 
 
-@pytest.mark.parametrize("mnk", [(128, 128, 16), (256, 384, 512), (200, 130, 66), (1024, 2048, 512)])
+@pytest.mark.parametrize("mnk", [(128, 128, 16), (256, 384, 512), (200, 130, 66), (1024, 2048, 512),
+                                 (45, 90, 45), (129, 77, 33), (1, 1, 1), (3, 5, 0)])
 def test_dgemm_accumulate_rel_l2(mnk):
     import torch
 
@@ -70,3 +71,21 @@ def test_dgemm_submatrix_views_and_forward():
     want = A[:, ns:2 * ns].cpu().numpy() @ B.cpu().numpy()
     err = np.linalg.norm(C.cpu().numpy() - want) / np.linalg.norm(want)
     assert err <= 1e-12
+
+
+def test_dgemm_unaligned_views():
+    """Operands that start at an odd element offset (8-byte aligned only) and
+    odd leading dimensions take the 8-byte-copy variant of the same kernel."""
+    import torch
+
+    from paper_2506_02486_b200 import gemm
+    g = torch.Generator(device="cuda").manual_seed(11)
+    big = torch.rand(300, 301, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    A = big[1:130, 3:70]          # 129 x 67, ld 301, base offset odd
+    B = big[5:72, 101:240]        # 67 x 139
+    C0 = torch.rand(129, 139, dtype=torch.float64, device="cuda", generator=g)
+    C = C0.clone()
+    gemm.dgemm_accumulate(A, B, C)
+    want = C0.cpu().numpy() + A.cpu().numpy() @ B.cpu().numpy()
+    err = np.linalg.norm(C.cpu().numpy() - want) / np.linalg.norm(want)
+    assert err <= 1e-12, err

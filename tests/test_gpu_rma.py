@@ -47,6 +47,45 @@ def test_roundtrips_two_ranks():
     assert run_emulated(2, roundtrip_worker, segment_bytes=32 * MIB) == [True, True]
 
 
+@pytest.mark.parametrize("size", [65536 + 5, 16 * MIB + 3, 16 * MIB + 4096])
+@pytest.mark.parametrize("offs", [(0, 0), (3, 3), (5, 9)])
+def test_remote_engines_byte_exact(size, offs, monkeypatch):
+    """The engines a peer GPU selects -- copy-engine put (>= 64 KiB) and the
+    bulk-async TMA get (>= 16 MiB, same alignment mod 16) -- forced on this box
+    (DIOMP_FORCE_REMOTE=1), byte-exact incl. unaligned heads/tails and the
+    misaligned-pair fallback."""
+    import torch
+
+    import paper_2506_02486_b200 as d
+    from paper_2506_02486_b200.emulate import run_emulated
+    monkeypatch.setenv("DIOMP_FORCE_REMOTE", "1")
+    so, do = offs
+
+    def fn(rt):
+        src = rt.alloc_symmetric(size + 64, 0)
+        dst = rt.alloc_symmetric(size + 64, 0)
+        back = rt.alloc_symmetric(size + 64, 0)
+        ok = True
+        if rt.rank == 0:
+            arena = rt.gm.arena(0)
+            g = torch.Generator(device=arena.device).manual_seed(size + so)
+            data = torch.randint(0, 256, (size,), dtype=torch.uint8, device=arena.device,
+                                 generator=g)
+            arena[src.addr.offset + so:src.addr.offset + so + size] = data
+            torch.cuda.synchronize(arena.device)
+            rt.put(d.GlobalAddress(1, 0, dst.addr.offset + do),
+                   d.GlobalAddress(0, 0, src.addr.offset + so), size, d.TransferKind.D2D)
+            rt.fence(rt.world)
+            rt.get(d.GlobalAddress(1, 0, dst.addr.offset + do),
+                   d.GlobalAddress(0, 0, back.addr.offset + so), size, d.TransferKind.D2D).wait(30)
+            got = arena[back.addr.offset + so:back.addr.offset + so + size]
+            ok = bool(torch.equal(got, data))
+        rt.barrier(rt.world)
+        return ok
+
+    assert run_emulated(2, fn, segment_bytes=256 * MIB) == [True, True]
+
+
 def test_misaligned_offsets_byte_exact():
     import paper_2506_02486_b200 as d
     from paper_2506_02486_b200.emulate import run_emulated

@@ -57,6 +57,37 @@ def test_multi_rank_decomposition_independence(key, ranks):
     assert _run(*key, ranks=ranks) == CASES[key]["sha256"]
 
 
+@pytest.mark.parametrize("key,ranks", [((16, 12, 12, 4, 1.0), 2), ((24, 20, 18, 7, 1.0), 3),
+                                       ((64, 64, 64, 100, 1.0), 2), ((64, 64, 64, 100, 1.0), 4),
+                                       ((128, 128, 128, 100, 1.0), 2)])
+def test_fused_epilogue_halo_stores_host_ordered(key, ranks):
+    """The fused kernel's halo epilogue (u_next planes stored straight into the
+    neighbours' ghost planes, csrc/stencil.cuh) with the steps ordered by a
+    host barrier instead of device flags (mode fused_host): runs wherever the
+    ranks sit, so a one-GPU box checks the peer-store epilogue too --
+    including BASELINE configs[0] (128^3, 2 ranks, 100 steps)."""
+    assert _run(*key, ranks=ranks, mode="fused_host") == CASES[key]["sha256"]
+
+
+def test_fused_host_refuses_generic_shapes():
+    """Odd NZ has no TMA fast path; without device flags the generic path could
+    not order its halo stores, so the library refuses rather than race."""
+    from paper_2506_02486_b200.apps.stencil import StencilRunner, StencilSpec
+    from paper_2506_02486_b200.emulate import run_emulated
+    from paper_2506_02486_b200.errors import DiompError
+
+    def fn(rt):
+        r = StencilRunner(rt, StencilSpec(16, 12, 13, steps=1), mode="fused_host")
+        rt.barrier(rt.world)
+        try:
+            r.run(1)
+        except DiompError:
+            return "refused"
+        return "ran"
+
+    assert run_emulated(2, fn, segment_bytes=_seg_bytes(16, 12, 13, 2)) == ["refused"] * 2
+
+
 @pytest.mark.parametrize("key,ranks", [((16, 12, 12, 4, 1.0), 2), ((24, 20, 18, 7, 1.0), 3)])
 def test_twosided_mailbox_exchange(key, ranks):
     """exchange="twosided" (reference halo_twosided.py): mailbox puts, delivery
