@@ -30,7 +30,7 @@ import numpy as np
 
 from .. import _native, gemm, kernels
 from ..errors import ShapeMismatch
-from ..runtime import COUNTER_GEMM, Runtime
+from ..runtime import CHANNEL_GEMM, COUNTER_GEMM, Runtime
 
 
 @dataclass(frozen=True)
@@ -164,12 +164,12 @@ class CannonRing:
                 sync = dict(wait_addr=[], wait_value=[], sig_addr=[], sig_value=[],
                             counter=rt.counter_address(d, COUNTER_GEMM))
                 for nb, idx in nbrs:
-                    sent, recvd = rt.pair_epochs(me, idx)
-                    sync["wait_addr"].append(rt.flag_address(ep.rank, d, idx))
+                    sent, recvd = rt.pair_epochs(me, idx, CHANNEL_GEMM)
+                    sync["wait_addr"].append(rt.flag_address(ep.rank, d, idx, CHANNEL_GEMM))
                     sync["wait_value"].append(recvd)
-                    sync["sig_addr"].append(rt.flag_address(nb.rank, nb.device, me))
+                    sync["sig_addr"].append(rt.flag_address(nb.rank, nb.device, me, CHANNEL_GEMM))
                     sync["sig_value"].append(sent + 1)
-                    rt.advance_pair(me, idx, 1)
+                    rt.advance_pair(me, idx, 1, CHANNEL_GEMM)
             src = rt.gm.base(d) + cur_rec.addr.offset
             if self.shift == "ce":
                 self._ce_step(st["gpu"], d, ns, n, a_blk, src, st["c"], fwd, sync)

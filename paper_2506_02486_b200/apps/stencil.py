@@ -33,7 +33,7 @@ import numpy as np
 from .. import _native
 from ..errors import DecompositionError, UsageError
 from ..global_memory import GlobalAddress, TransferKind
-from ..runtime import COUNTER_STENCIL, Runtime
+from ..runtime import CHANNEL_STENCIL, COUNTER_STENCIL, Runtime
 from . import halo_onesided, halo_twosided
 
 VELOCITY = 1500.0
@@ -149,9 +149,9 @@ class StencilRunner:
                 if nb is None:
                     continue
                 nb_idx = rt.endpoint_index(nb, 0)
-                sent, recvd = rt.pair_epochs(self.me_idx, nb_idx)
-                setattr(p, f"wait_{side}", rt.flag_address(rt.rank, 0, nb_idx))
-                setattr(p, f"sig_{side}", rt.flag_address(nb, 0, self.me_idx))
+                sent, recvd = rt.pair_epochs(self.me_idx, nb_idx, CHANNEL_STENCIL)
+                setattr(p, f"wait_{side}", rt.flag_address(rt.rank, 0, nb_idx, CHANNEL_STENCIL))
+                setattr(p, f"sig_{side}", rt.flag_address(nb, 0, self.me_idx, CHANNEL_STENCIL))
                 setattr(p, f"from_{side}", recvd)
                 setattr(p, f"to_{side}", sent)
             p.counter = rt.counter_address(0, COUNTER_STENCIL)
@@ -168,7 +168,8 @@ class StencilRunner:
             for nb in (self.left, self.right):
                 if nb is not None:
                     # nsteps + 1 signals per call: entry + one per step
-                    self.rt.advance_pair(self.me_idx, self.rt.endpoint_index(nb, 0), nsteps + 1)
+                    self.rt.advance_pair(self.me_idx, self.rt.endpoint_index(nb, 0), nsteps + 1,
+                                         CHANNEL_STENCIL)
         self.step += nsteps
 
     def run(self, nsteps: int):

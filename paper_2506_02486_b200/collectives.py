@@ -29,7 +29,7 @@ import numpy as np
 from . import _native
 from .errors import InvalidAddress, RootOutOfRange, StaleGroup, TypeMismatch, UsageError
 from .global_memory import GlobalAddress
-from .runtime import COUNTER_COLL, COUNTER_OFF, Group, Runtime
+from .runtime import CHANNEL_COLL, COUNTER_COLL, COUNTER_OFF, Group, Runtime
 from .topology import Endpoint
 
 
@@ -145,7 +145,7 @@ def _team(comm: Communicator, pos: int, sync: int) -> _native.Team:
         t = _native.Team()
         t.k, t.pos, t.sync = comm.size, pos, sync
         t.device = rt.gpus[me_ep.device]
-        t.flag_off = rt.flag_offset
+        t.flag_off = rt.channel_flag_offset(CHANNEL_COLL)
         t.counter_off = rt.scratch_offset + COUNTER_OFF + 64 * COUNTER_COLL
         for q, ep in enumerate(comm.ring):
             t.base[q] = rt.peer_address(ep.rank, ep.device)
@@ -153,7 +153,7 @@ def _team(comm: Communicator, pos: int, sync: int) -> _native.Team:
         cache[(pos, sync)] = t
     for q in range(comm.size):
         if q != pos:
-            t.epoch_to[q], t.epoch_from[q] = rt.pair_epochs(me, t.slot[q])
+            t.epoch_to[q], t.epoch_from[q] = rt.pair_epochs(me, t.slot[q], CHANNEL_COLL)
     return t
 
 
@@ -196,7 +196,8 @@ def _run(comm: Communicator, launch, blocking: bool = True, signals: int = 2):
             me = rt.endpoint_index(me_ep.rank, me_ep.device)
             for q, ep in enumerate(comm.ring):
                 if q != pos:
-                    rt.advance_pair(me, rt.endpoint_index(ep.rank, ep.device), signals)
+                    rt.advance_pair(me, rt.endpoint_index(ep.rank, ep.device), signals,
+                                    CHANNEL_COLL)
     elif comm.size > 1:
         rt.barrier(comm.group)
 
