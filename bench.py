@@ -33,6 +33,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 GRID = int(os.environ.get("BENCH_GRID", "1024"))
+GEMM_N = int(os.environ.get("BENCH_GEMM_N", "16384"))
 FALLBACK_HBM_GBS = 6650.0
 E2E_MIN_STEPS = 100
 
@@ -223,6 +224,20 @@ def run_reference_arm(args):
     finally:
         ref.close()
     value = statistics.median(vals)
+    sec = {}
+    if not args.no_secondary:
+        sec = {"minimod_128": {"workload": "minimod_128^3_100steps", "ranks": 2}}
+        if world >= 2:
+            sec["p2p"] = {"value": 0.0}
+            sec["collectives"] = {"allreduce": {}}
+        if world == 1:
+            sec["dgemm_ring"] = {"value": 0.0, "workload": f"cannon_ring_{GEMM_N}^2_fp64"}
+        sec["minimod_128"]["value"] = 0.0
+        _secondary_cpu(sec, world)
+        for v in sec.values():   # the CPU arm's own numbers are the values
+            if isinstance(v, dict) and "cpu_baseline" in v:
+                v["value"] = v["cpu_baseline"]["value"]
+                v["unit"] = v["cpu_baseline"]["unit"]
     line = {"metric": "minimod_gpts_per_s", "value": round(value, 4), "unit": "Gpts/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
@@ -232,6 +247,8 @@ def run_reference_arm(args):
             "impl": "reference", "cpu_baseline": ref.describe(value, args.steps),
             "e2e": {"value": round(value, 4), "unit": "Gpts/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    if sec:
+        line["secondary"] = sec
     print(json.dumps(line), flush=True)
     return 0
 
@@ -240,10 +257,17 @@ def run_reference_arm(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def _secondary_bytes(world: int) -> int:
+    """Segment room for the secondary measurements (linear heap, no reuse
+    across sizes): two DGEMM ring stripes + the 1 GiB p2p / collective pair."""
+    ns = GEMM_N // world
+    return 2 * ns * GEMM_N * 8 + (2 << 30) + (256 << 20)
+
+
 def _make_runtime(world: int, rank: int, local: int, field_bytes: int):
     from paper_2506_02486_b200 import (AllocatorKind, LaunchConfig, SegmentConfig, runtime)
     from paper_2506_02486_b200.config import resolve_from_env
-    need = (2 * field_bytes + (64 << 20)) * 4 // 3
+    need = (2 * field_bytes + (64 << 20) + _secondary_bytes(world)) * 4 // 3
     seg = 1 << max(24, (need - 1).bit_length())
     os.environ.setdefault("DIOMP_GPUS", str(local))
     cfg = resolve_from_env(LaunchConfig(nranks=world, segment=SegmentConfig(
@@ -313,6 +337,7 @@ def run_stencil_bench(args):
     # one stencil kernel per step; with neighbours, one one-thread signal
     # kernel per neighbour after the last step (rank 0: right only)
     launches = args.steps + (1 if world > 1 else 0)
+    secondary = None if args.no_secondary else _secondary(rt, rank, world)
     if rank == 0:
         line = {"metric": "minimod_gpts_per_s", "value": round(value, 3), "unit": "Gpts/s",
                 "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
@@ -333,9 +358,81 @@ def run_stencil_bench(args):
                 line["cpu_baseline"] = cpu_baseline(GRID)
             except Exception as e:  # report, do not fail the GPU number
                 line["cpu_baseline"] = {"error": str(e)[:200]}
+        if secondary is not None:
+            if not args.no_cpu:
+                _secondary_cpu(secondary, world)
+            line["secondary"] = secondary
         print(json.dumps(line), flush=True)
     rt.finalize()
     return 0
+
+
+def _secondary(rt, rank, world):
+    """The other BASELINE configs, measured in the same run on the same
+    runtime (after the headline's fields are freed): configs[0] Minimod 128^3
+    x 100 steps, configs[3] the 16384^2 fp64 ring (reference inputs and a
+    host-BLAS rel-L2 at one GPU), and at >= 2 GPUs configs[1] put/get and
+    configs[2] allreduce / bcast at 64 MiB and 1 GiB."""
+    from paper_2506_02486_b200.apps import bench as appbench
+    out = {}
+    for name, fn in (("minimod_128", lambda: appbench.measure_stencil_config1(rt)),
+                     ("dgemm_ring", lambda: appbench.measure_dgemm_ring(rt, GEMM_N)),
+                     ("p2p", lambda: appbench.measure_p2p(rt)),
+                     ("collectives", lambda: appbench.measure_collectives(rt))):
+        try:
+            v = fn()
+        except Exception as e:   # report, do not lose the headline
+            v = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+        if v is not None and rank == 0:
+            out[name] = v
+    if rank == 0 and "minimod_128" in out and "sha256" in out["minimod_128"]:
+        try:
+            gold = json.load(open(os.path.join(HERE, "tests", "golden", "stencil_golden.json")))
+            want = [c["sha256"] for c in gold["cases"]
+                    if (c["nx"], c["steps"], c["amp"]) == (128, 100, 1.0)][0]
+            out["minimod_128"]["matches_reference_sha256"] = out["minimod_128"]["sha256"] == want
+        except Exception:
+            pass
+    return out if rank == 0 else None
+
+
+def _secondary_cpu(sec, world):
+    """cpu_baseline of each secondary entry: the oracle's multi-process
+    restatements of the reference's drivers (oracle/ports.py) on the host."""
+    from oracle import ports as P
+    try:
+        if "minimod_128" in sec and "value" in sec["minimod_128"]:
+            r = P.stencil_procs(128, 128, 128, 100, 2, checksum=False)
+            sec["minimod_128"]["cpu_baseline"] = {
+                "value": round(r["gpts"], 4), "unit": "Gpts/s", "cores": 2, "kind": r["kernel"],
+                "seconds": round(r["seconds"], 3),
+                "sample": "the whole config: run_stencil 128^3 x 100 steps on 2 processes "
+                          "(shared-memory halo puts + barrier, the reference's compiled "
+                          "stencil_update)"}
+        if "dgemm_ring" in sec and "value" in sec["dgemm_ring"] and world == 1:
+            from paper_2506_02486_b200.apps import bench as appbench
+            sec["dgemm_ring"]["cpu_baseline"] = appbench._cpu_dgemm_sample(GEMM_N)
+        if sec.get("p2p") and "value" in sec["p2p"]:
+            r = P.p2p_sample()
+            sec["p2p"]["cpu_baseline"] = {
+                "value": round(r["put_bandwidth_gbs"], 3), "unit": "GB/s", "cores": 2,
+                "kind": "port", "put_latency_us_8B": round(r["put_latency_us_8B"], 2),
+                "get_latency_us_8B": round(r["get_latency_us_8B"], 2),
+                "get_bandwidth_gbs": round(r["get_bandwidth_gbs"], 3),
+                "sample": "2 processes, loopback TCP with the reference's wire frames "
+                          "(oracle/ports.WirePair): 8 x 64 MiB puts + fence, 200 x 8 B"}
+        if sec.get("collectives") and "allreduce" in sec["collectives"]:
+            cb = {}
+            for op in ("allreduce", "bcast"):
+                r = P.ring_collective(op, world, 64 << 20, iters=3, check=False)
+                cb[op] = round(r["busbw_gbs"], 4)
+            sec["collectives"]["cpu_baseline"] = {
+                "value": cb["allreduce"], "unit": "GB/s (busBW)", "cores": world, "kind": "port",
+                "bcast": cb["bcast"],
+                "sample": f"{world} processes in a loopback-TCP ring (oracle/ports), 64 MiB, "
+                          "3 reps each"}
+    except Exception as e:
+        sec["cpu_baseline_error"] = str(e)[:300]
 
 
 def _stencil_e2e(rt, spec, steps, field_bytes):
@@ -379,6 +476,7 @@ def main():
     ap.add_argument("--workload", default="stencil")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -465,6 +465,189 @@ def _cpu_dgemm_sample(n: int) -> dict:
                       f"at P=16), default BLAS threads"}
 
 
+# ---------------------------------------------------------------------------
+# secondary measurements (the other BASELINE configs, reported in the
+# headline line of bench.py next to the Minimod 1024^3 number)
+# ---------------------------------------------------------------------------
+
+def _max_over_ranks(rt, tag: str, value: float) -> float:
+    got = rt.ctrl.allgather(tuple(range(rt.nranks)), tag, pickle.dumps(value))
+    return max(pickle.loads(b) for _, b in got)
+
+
+def measure_stencil_config1(rt: Runtime, n: int = 128, steps: int = 100) -> dict:
+    """BASELINE configs[0] (Minimod n^3, `steps` steps; the reference runs it on
+    2 ranks) on this job's ranks through the public StencilRunner: device time
+    of the whole run (CUDA events, max over ranks), the end-to-end time with
+    the zero initial fields copied H2D from pinned host memory and the final
+    field D2H inside the timed region, and the sha256 of the gathered field."""
+    import hashlib
+
+    import torch
+
+    from .stencil import StencilRunner, StencilSpec, _gather_field, dump_bytes
+    spec = StencilSpec(n, n, n, steps=steps)
+    runner = StencilRunner(rt, spec)
+    timer = _Timer(rt)
+    rt.barrier(rt.world)
+    timer.stream = runner.stream.handle
+    timer.start()
+    runner.enqueue(steps) if runner.mode == "fused" else runner.run(steps)
+    dev_s = _max_over_ranks(rt, "cfg1/dev", timer.stop_ms() / 1e3)
+    _native.check_device(runner.gpu, "stencil config1")
+    rt.barrier(rt.world)
+    field = _gather_field(rt, runner.cur_rec, spec, runner.nxl, runner.shape)
+    sha = hashlib.sha256(dump_bytes(field)).hexdigest() if rt.rank == 0 else ""
+    # end to end: fresh fields from host, run, result back to host
+    host_in = torch.zeros(runner.nbytes // 8, dtype=torch.float64).pin_memory()
+    host_out = torch.empty(runner.nbytes // 8, dtype=torch.float64).pin_memory()
+    base, s = rt.gm.base(0), runner.stream.handle
+    runner.step = 0
+    rt.barrier(rt.world)
+    t0 = time.perf_counter()
+    for rec in (runner.field_a, runner.field_b):
+        _native.call("diomp_memcpy_async", base + rec.addr.offset, host_in.data_ptr(),
+                     runner.nbytes, 1, s)
+    runner.enqueue(steps) if runner.mode == "fused" else runner.run(steps)
+    _native.call("diomp_memcpy_async", host_out.data_ptr(), base + runner.cur_rec.addr.offset,
+                 runner.nbytes, 2, s)
+    runner.stream.synchronize()
+    rt.barrier(rt.world)
+    e2e_s = _max_over_ranks(rt, "cfg1/e2e", time.perf_counter() - t0)
+    mode = runner.mode
+    runner.free()
+    pts = float(n) ** 3 * steps
+    return {"workload": f"minimod_{n}^3_{steps}steps", "ranks": rt.nranks, "mode": mode,
+            "value": round(pts / dev_s / 1e9, 3), "unit": "Gpts/s",
+            "seconds": round(dev_s, 6), "sha256": sha,
+            "e2e": {"value": round(pts / e2e_s / 1e9, 3), "unit": "Gpts/s",
+                    "seconds": round(e2e_s, 6),
+                    "h2d_bytes": 2 * runner.nbytes * rt.nranks,
+                    "d2h_bytes": runner.nbytes * rt.nranks}}
+
+
+def measure_dgemm_ring(rt: Runtime, n: int = 16384, reps: int = 3, host_check: bool = True):
+    """BASELINE configs[3]: the n x n fp64 ring multiply on this job's
+    endpoints.  Device time per multiply (best of `reps`, max over ranks), the
+    cuBLAS DGEMM time of the same per-endpoint products without the shift,
+    and -- at one rank with host_check -- the reference's inputs
+    (_fill_matrices(n, 0)), the end-to-end time (A, B pinned H2D, the ring,
+    C D2H) and rel-L2 of C against host BLAS (numpy a @ b, cannon.py:138)."""
+    import torch
+
+    from .cannon import CannonRing, MatmulSpec, _fill_matrices
+    spec = MatmulSpec(n, rt.nranks)
+    host = host_check and rt.nranks == 1
+    a = b = None
+    if host:
+        a, b = _fill_matrices(n, 0)
+        ring = CannonRing(rt, spec, a_full=a, b_full=b)
+    else:
+        ring = CannonRing(rt, spec, device_seed=0)
+    timer = _Timer(rt)
+    timer.stream = ring._stream(0)
+
+    def one():
+        for _ in range(spec.p):
+            ring.enqueue_step() if ring.sync else ring.run()
+
+    out = {"workload": f"cannon_ring_{n}^2_fp64", "endpoints": spec.p,
+           "kernel": "DMMA m8n8k4", "shift": ring.shift if spec.p > 1 else None}
+    if host:
+        (e, st), = ring.local.items()
+        pa = torch.from_numpy(a).pin_memory()
+        pb = torch.from_numpy(b).pin_memory()
+        pc = torch.empty(n, n, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st["a"].copy_(pa, non_blocking=True)
+        ring.stripe(st["dev"], 0).copy_(pb, non_blocking=True)
+        st["c"].zero_()
+        torch.cuda.synchronize()
+        ring.step_no = 0
+        one()
+        ring.synchronize()
+        pc.copy_(st["c"], non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        got = pc.numpy()
+        want = a @ b
+        out["rel_l2_vs_host_blas"] = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+        out["e2e"] = {"value": round(2.0 * n ** 3 / e2e_s / 1e12, 3), "unit": "TFLOP/s",
+                      "seconds": round(e2e_s, 4), "h2d_bytes": 2 * n * n * 8,
+                      "d2h_bytes": n * n * 8}
+        del pa, pb, pc, got, want
+    ms = []
+    rt.barrier(rt.world)
+    for _ in range(reps):
+        rt.barrier(rt.world)
+        timer.start()
+        one()
+        ms.append(timer.stop_ms())
+        ring.synchronize()
+    t = _max_over_ranks(rt, "gemm/dev", min(ms)) / 1e3
+    ring.release()
+
+    class _A:
+        steps = reps
+    t_cublas = _max_over_ranks(rt, "gemm/cublas", _cublas_same_shapes(rt, spec, _A))
+    tflops = 2.0 * n ** 3 / t / 1e12
+    out.update({"value": round(tflops, 3), "unit": "TFLOP/s", "ms_per_multiply": round(t * 1e3, 3),
+                "cublas_same_shapes_tflops": round(2.0 * n ** 3 / t_cublas / 1e12, 3),
+                "frac_of_cublas": round(t_cublas / t, 4)})
+    return out
+
+
+def measure_p2p(rt: Runtime, sizes=(8, 64 * MIB, 1 << 30), iters: int = 5) -> dict | None:
+    """BASELINE configs[1] legs between rank 0 and rank 1: D2D put / get
+    bandwidth (device-timed), 8 B put+fence and get+wait latency (host API),
+    and the end-to-end put with a HOST payload (kind H2D, the reference's
+    default) at the largest size."""
+    if rt.nranks < 2:
+        return None
+    big = [x for x in sizes if x >= MIB]
+    res = {}
+    for kind in (BenchKind.Bandwidth, BenchKind.GetBandwidth):
+        rows = run_p2p(rt, BenchSpec(kind, tuple(big), iters=iters, warmup=2,
+                                     transfer=TransferKind.D2D))
+        res[kind.value] = {r.size_bytes: round(r.size_bytes / r.mean_us / 1e3, 2) for r in rows}
+    for kind in (BenchKind.PutLatency, BenchKind.GetLatency):
+        rows = run_p2p(rt, BenchSpec(kind, (8,), iters=200, warmup=20, transfer=TransferKind.D2D))
+        res[kind.value] = {r.size_bytes: round(r.mean_us, 2) for r in rows}
+    rows = run_p2p(rt, BenchSpec(BenchKind.Bandwidth, (max(big),), iters=2, warmup=1))
+    res["bw_h2d"] = {r.size_bytes: round(r.size_bytes / r.mean_us / 1e3, 2) for r in rows}
+    if rt.rank != 0:
+        return None
+    top = max(big)
+    return {"workload": "p2p_rank0_rank1", "unit": "GB/s",
+            "put_bw": res["bw"], "get_bw": res["get_bw"],
+            "put_latency_us_8B": res["put"].get(8), "get_latency_us_8B": res["get"].get(8),
+            "value": res["bw"][top], "frac_of_peer_copy": round(res["bw"][top] / NVLINK_PEER_GBS, 4),
+            "e2e": {"value": res["bw_h2d"][top], "unit": "GB/s", "h2d_bytes": top,
+                    "d2h_bytes": 0, "note": "put with a host payload (TransferKind.H2D)"}}
+
+
+def measure_collectives(rt: Runtime, sizes=(64 * MIB, 1 << 30), iters: int = 5) -> dict | None:
+    """BASELINE configs[2] top sizes: allreduce (f32 sum, exact fold) and bcast
+    busBW over every rank, device-timed, max over ranks."""
+    if rt.nranks < 2:
+        return None
+    out = {}
+    comm = coll.bootstrap(rt, rt.world)
+    k = rt.nranks
+    for kind in (BenchKind.Allreduce, BenchKind.Bcast):
+        rows = run_collective(rt, BenchSpec(kind, tuple(sizes), iters=iters, warmup=2), comm)
+        f = 2 * (k - 1) / k if kind is BenchKind.Allreduce else 1.0
+        out[kind.value] = {r.size_bytes: round(f * r.size_bytes / r.mean_us / 1e3, 2)
+                           for r in rows}
+    if rt.rank != 0:
+        return None
+    return {"workload": f"collectives_k{k}", "unit": "GB/s (busBW)",
+            "allreduce": out["allreduce"], "bcast": out["bcast"],
+            "frac_of_peer_copy_64MiB": {kk: round(v[64 * MIB] / NVLINK_PEER_GBS, 4)
+                                        for kk, v in out.items() if 64 * MIB in v}}
+
+
 def cli_bench(args) -> int:
     if args.workload == "p2p":
         return _p2p_cli(args)

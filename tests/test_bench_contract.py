@@ -31,6 +31,11 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
+    # the other BASELINE configs' CPU paths, timed in the same run
+    sec = d["secondary"]
+    assert sec["minimod_128"]["cpu_baseline"]["value"] > 0
+    assert sec["minimod_128"]["cpu_baseline"]["cores"] == 2
+    assert sec["dgemm_ring"]["cpu_baseline"]["unit"] == "TFLOP/s"
 
 
 def test_reference_arm_non_zero_ranks_exit_quietly():
