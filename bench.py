@@ -483,7 +483,40 @@ def main():
     if args.workload == "stencil":
         return run_stencil_bench(args)
     from paper_2506_02486_b200.apps import bench as appbench
+    if not args.no_cpu:
+        appbench._LINE_HOOK = _cli_cpu_hook
     return appbench.cli_bench(args)
+
+
+def _cli_cpu_hook(d):
+    """cpu_baseline for the --workload lines: the oracle's restatement of the
+    reference's own CPU path for that config (oracle/ports.py), on rank 0."""
+    from oracle import ports as P
+    world = d.get("n_gpus", 1)
+    try:
+        if d["metric"].startswith("put_bandwidth"):
+            r = P.p2p_sample()
+            d["cpu_baseline"] = {"value": round(r["put_bandwidth_gbs"], 3), "unit": "GB/s",
+                                 "cores": 2, "kind": "port",
+                                 "put_latency_us_8B": round(r["put_latency_us_8B"], 2),
+                                 "get_latency_us_8B": round(r["get_latency_us_8B"], 2),
+                                 "get_bandwidth_gbs": round(r["get_bandwidth_gbs"], 3),
+                                 "sample": "2 processes, loopback TCP, the reference's wire "
+                                           "frames: 8 x 64 MiB puts + fence; 200 x 8 B"}
+        elif d["metric"].startswith(("allreduce", "bcast")):
+            op = "allreduce" if d["metric"].startswith("allreduce") else "bcast"
+            rows = []
+            for nbytes in (1 << 20, 64 << 20):
+                r = P.ring_collective(op, world, nbytes, iters=3, check=False)
+                rows.append((nbytes, round(r["seconds"] * 1e6, 1), round(r["busbw_gbs"], 4)))
+            d["cpu_baseline"] = {"value": rows[-1][2], "unit": "GB/s (busBW)", "cores": world,
+                                 "kind": "port", "rows": rows,
+                                 "sample": f"{world} processes, loopback-TCP ring "
+                                           "(oracle/ports.ring_collective), 1 MiB and 64 MiB"}
+        elif d["metric"].startswith("dgemm") and world == 1:
+            pass   # already attached (OpenBLAS sample) by the dgemm CLI
+    except Exception as e:
+        d["cpu_baseline"] = {"error": str(e)[:300]}
 
 
 if __name__ == "__main__":

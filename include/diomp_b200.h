@@ -102,6 +102,40 @@ int diomp_copy(int device, uint64_t dst, uint64_t src, uint64_t nbytes, void *st
  * the bulk-async TMA kernel, everything else on the SM copy kernel.          */
 int diomp_put(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int remote, void *stream);
 int diomp_get(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int remote, void *stream);
+/* ---- rank-addressed RMA context: what a C / Cython caller binds
+ *      to reach the global address space without Python.
+ *      A context holds the peer table -- every endpoint's segment base as
+ *      mapped in this process (CUDA IPC / peer access; global_memory.py:73-84
+ *      GlobalAddress -> arena) -- and the ops in flight.  An endpoint is
+ *      rank * devices_per_rank + dev (topology.py endpoint index).
+ *      put/get replace runtime.py:371-470 -> transport.py:508-566 and return
+ *      an op handle (transport.py:58-101 CompletionHandle): op_query ->
+ *      DIOMP_OK (RemoteDone) / DIOMP_PENDING, op_wait blocks (DIOMP_INTERNAL on
+ *      timeout), fence_group(mask) = runtime.py:535-556 fence toward a set of
+ *      endpoints.  Ranges are checked against the segment extent
+ *      (DIOMP_INVALID_ADDRESS); allocation-level checks (global_memory.py:
+ *      306-333) stay with the caller, as in the reference.                  */
+int diomp_rma_ctx_create(int32_t nranks, int32_t devices_per_rank, void **ctx_out);
+int diomp_rma_ctx_destroy(void *ctx);
+/* local device index -> CUDA device ordinal; phys_gpu = box-wide GPU id
+ * (two endpoints on the same phys_gpu are local copies, others cross NVLink) */
+int diomp_rma_set_local(void *ctx, int32_t local_dev, int32_t cuda_device, int32_t phys_gpu);
+int diomp_rma_set_force_remote(void *ctx, int32_t on); /* test knob: take the NVLink engines */
+int diomp_peer_table_set(void *ctx, int32_t rank, int32_t dev, uint64_t base, uint64_t bytes,
+                         int32_t phys_gpu);
+/* kind DIOMP_H2D (src = host pointer) or DIOMP_D2D (src = device pointer on local_dev) */
+int diomp_rma_put(void *ctx, int32_t dst_rank, int32_t dst_dev, uint64_t dst_off, uint64_t src,
+                  uint64_t nbytes, int32_t kind, int32_t local_dev, void *stream,
+                  uint64_t *op_out);
+/* kind DIOMP_D2H (dst = host pointer) or DIOMP_D2D (dst = device pointer on local_dev) */
+int diomp_rma_get(void *ctx, int32_t src_rank, int32_t src_dev, uint64_t src_off, uint64_t dst,
+                  uint64_t nbytes, int32_t kind, int32_t local_dev, void *stream,
+                  uint64_t *op_out);
+int diomp_op_query(void *ctx, uint64_t op);
+int diomp_op_wait(void *ctx, uint64_t op, double timeout_s);   /* timeout_s < 0: no limit */
+int diomp_fence_group(void *ctx, uint64_t endpoint_mask);
+int diomp_rma_outstanding(void *ctx, uint64_t endpoint_mask, uint64_t *count_out);
+
 /* host<->device legs of H2D put / D2H get (TransferKind, global_memory.py:52-70) */
 #define DIOMP_H2D 1
 #define DIOMP_D2H 2
@@ -149,10 +183,9 @@ int diomp_team_barrier(const diomp_team *team, void *stream);
  *      reference's ring folds:
  *        reduce:    root gets ((v_root op v_root+1) op ...) op v_root-1
  *        allreduce: block b=[b*count/k,(b+1)*count/k) folded from position b.
- * allreduce is one kernel (fold, store the block to every member); from
- * diomp_set_allreduce_ce_min() bytes (default never; DIOMP_AR_ALGO=ce: all)
- * the fold goes to the own recv and the copy engine pushes it to the peers.
- * Same bits either way.                                                      */
+ * allreduce is one kernel (fold, store the block to every member); bcast:
+ * every non-root pulls its 1/(k-1) block from the root and pushes it to the
+ * other non-roots.                                                           */
 #define DIOMP_F32 0
 #define DIOMP_F64 1
 #define DIOMP_I32 2
@@ -162,32 +195,27 @@ int diomp_team_barrier(const diomp_team *team, void *stream);
 #define DIOMP_MAX 2
 int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_t root,
                 void *stream);
-/* bcast algorithm switch: from `bytes` (default never; DIOMP_BCAST_CHAIN_MIN,
- * DIOMP_BCAST_ALGO=pull|chain) device-synchronised teams of k >= 3 use the
- * chain (root -> root+1 -> ... pipelined in chunks with per-CTA progress
- * flags, measured slower on B200); otherwise every non-root pulls its 1/(k-1)
- * block from the root and pushes it to the other non-roots.  Same bytes.    */
-int diomp_set_bcast_chain_min(uint64_t bytes);
-/* chain flavour for the sizes above: on = pull chain (every hop loads its chunk
- * from its predecessor over NVLink and stores it locally, so the per-chunk
- * fence drains local writes only), off = push chain (default;
- * DIOMP_BCAST_ALGO=pullchain sets on).                                       */
-int diomp_set_bcast_pullchain(int32_t on);
 int diomp_reduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
                  int32_t dtype, int32_t op, int32_t root, void *stream);
-int diomp_set_allreduce_ce_min(uint64_t bytes);
 int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off,
                     uint64_t count, int32_t dtype, int32_t op, void *stream);
 
-/* ---- NVSwitch multicast (NVLS) allreduce: collectives.allreduce
- *      (collectives.py:326-405) with the reduction done in the switch
- *      (multimem.ld_reduce) and the result fanned out by one multimem.st.
- *      Float sums agree with the reference fold within rounding (not
- *      bitwise); integer sum/min/max are exact; float min/max are refused.
- *      Setup (collective over the communicator): position 0 creates the
- *      multicast object and exports it as a POSIX fd (passed to the other
- *      processes over a Unix socket), every member imports it, adds its GPU,
- *      then (after a barrier) binds a window of its own HBM.                  */
+#ifdef DIOMP_EXPERIMENTS
+/* ---- Experiments build only (-DDIOMP_EXPERIMENTS; measured slower than the
+ *      defaults on B200, kept out of the product library).
+ * bcast chain (root -> root+1 -> ... pipelined in chunks with per-CTA
+ * progress flags) from `bytes` for teams of k >= 3; pull flavour = every hop
+ * loads from its predecessor.  allreduce with the copy engine pushing each
+ * folded block from `bytes`.  Same bytes as the defaults.                    */
+int diomp_set_bcast_chain_min(uint64_t bytes);
+int diomp_set_bcast_pullchain(int32_t on);
+int diomp_set_allreduce_ce_min(uint64_t bytes);
+/* NVSwitch multicast (NVLS) allreduce: the switch reduces (multimem.ld_reduce)
+ * and one multimem.st fans the result out.  Float sums agree with the
+ * reference fold within rounding (not bitwise); integer sum/min/max exact;
+ * float min/max refused.  Setup is collective over the communicator
+ * (position 0 creates the multicast object, exports a POSIX fd, members
+ * import, add their GPU, bind a window of their HBM).                      */
 int diomp_mc_supported(int device, int *out);
 int diomp_mc_window_bytes(int nmembers, uint64_t want, uint64_t *total_out);
 int diomp_mc_create(int nmembers, uint64_t total, int *fd_out, uint64_t *mc_out);
@@ -208,6 +236,7 @@ typedef struct {
 } diomp_nvls_args;
 int diomp_allreduce_nvls(const diomp_nvls_args *args, void *stream);
 int diomp_nvls_rounds(uint64_t count, int dtype, uint64_t window, uint64_t *rounds_out);
+#endif /* DIOMP_EXPERIMENTS */
 
 /* ---- Minimod stencil: kernels/__init__.py:30 seam `stencil_update`
  *      (reference.py:14-31 / _core.pyx:9-32).  One interior update of

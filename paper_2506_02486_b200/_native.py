@@ -98,6 +98,19 @@ _PROTOS = {
     "diomp_event_elapsed_ms": [c_vp, c_vp, ctypes.POINTER(ctypes.c_float)],
     "diomp_stream_wait_event": [c_vp, c_vp],
     "diomp_stream_query": [c_vp],
+    "diomp_rma_ctx_create": [c_i32, c_i32, ctypes.POINTER(c_vp)],
+    "diomp_rma_ctx_destroy": [c_vp],
+    "diomp_rma_set_local": [c_vp, c_i32, c_i32, c_i32],
+    "diomp_rma_set_force_remote": [c_vp, c_i32],
+    "diomp_peer_table_set": [c_vp, c_i32, c_i32, c_u64, c_u64, c_i32],
+    "diomp_rma_put": [c_vp, c_i32, c_i32, c_u64, c_u64, c_u64, c_i32, c_i32, c_vp,
+                      ctypes.POINTER(c_u64)],
+    "diomp_rma_get": [c_vp, c_i32, c_i32, c_u64, c_u64, c_u64, c_i32, c_i32, c_vp,
+                      ctypes.POINTER(c_u64)],
+    "diomp_op_query": [c_vp, c_u64],
+    "diomp_op_wait": [c_vp, c_u64, ctypes.c_double],
+    "diomp_fence_group": [c_vp, c_u64],
+    "diomp_rma_outstanding": [c_vp, c_u64, ctypes.POINTER(c_u64)],
     "diomp_copy": [ctypes.c_int, c_u64, c_u64, c_u64, c_vp],
     "diomp_put": [ctypes.c_int, c_u64, c_u64, c_u64, ctypes.c_int, c_vp],
     "diomp_get": [ctypes.c_int, c_u64, c_u64, c_u64, ctypes.c_int, c_vp],
@@ -108,9 +121,19 @@ _PROTOS = {
     "diomp_wait": [ctypes.c_int, c_u64, c_u64, c_vp],
     "diomp_team_barrier": [ctypes.POINTER(Team), c_vp],
     "diomp_bcast": [ctypes.POINTER(Team), c_u64, c_u64, c_i32, c_vp],
+    "diomp_reduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_i32, c_vp],
+    "diomp_allreduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_vp],
+    "diomp_stencil_update": [ctypes.c_int, ctypes.POINTER(StencilArgs), c_vp],
+    "diomp_stencil_run": [ctypes.POINTER(StencilPlan), c_i64, c_i64, c_vp],
+    "diomp_matmul_f64": [ctypes.c_int, c_i64, c_i64, c_i64, c_u64, c_u64, c_u64, c_vp],
+    "diomp_dgemm": [ctypes.POINTER(DgemmArgs), c_vp],
+}
+
+# experiments build only (-DDIOMP_EXPERIMENTS, include/diomp_b200.h): bound
+# when the loaded library has them
+_EXPERIMENTAL_PROTOS = {
     "diomp_set_bcast_chain_min": [c_u64],
     "diomp_set_bcast_pullchain": [c_i32],
-    "diomp_reduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_i32, c_vp],
     "diomp_set_allreduce_ce_min": [c_u64],
     "diomp_mc_supported": [ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
     "diomp_mc_window_bytes": [ctypes.c_int, c_u64, ctypes.POINTER(c_u64)],
@@ -122,14 +145,10 @@ _PROTOS = {
     "diomp_mc_release": [c_u64, ctypes.c_int, c_u64, c_u64, c_u64, c_u64],
     "diomp_allreduce_nvls": [ctypes.POINTER(NvlsArgs), c_vp],
     "diomp_nvls_rounds": [c_u64, ctypes.c_int, c_u64, ctypes.POINTER(c_u64)],
-    "diomp_allreduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_vp],
-    "diomp_stencil_update": [ctypes.c_int, ctypes.POINTER(StencilArgs), c_vp],
-    "diomp_stencil_run": [ctypes.POINTER(StencilPlan), c_i64, c_i64, c_vp],
-    "diomp_matmul_f64": [ctypes.c_int, c_i64, c_i64, c_i64, c_u64, c_u64, c_u64, c_vp],
-    "diomp_dgemm": [ctypes.POINTER(DgemmArgs), c_vp],
 }
 
-# symbols declared in include/diomp_b200.h (checked by tests/test_native_abi.py)
+# symbols declared in include/diomp_b200.h outside DIOMP_EXPERIMENTS (checked
+# by tests/test_native_abi.py)
 EXPORTS = sorted(list(_PROTOS) + ["diomp_status_string"])
 
 
@@ -143,12 +162,22 @@ def _load():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int
+    for name, args in _EXPERIMENTAL_PROTOS.items():
+        fn = getattr(lib, name, None)
+        if fn is not None:
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
     lib.diomp_status_string.argtypes = [ctypes.c_int]
     lib.diomp_status_string.restype = ctypes.c_char_p
     return lib
 
 
 lib = _load()
+
+
+def has_experiments() -> bool:
+    """True when the loaded library is an experiments build."""
+    return hasattr(lib, "diomp_allreduce_nvls")
 
 
 def describe(status: int) -> str:

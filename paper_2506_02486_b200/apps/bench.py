@@ -265,11 +265,16 @@ def _cli_runtime(seg_bytes: int):
     return Runtime(cfg)
 
 
+_LINE_HOOK = None   # bench.py sets this to attach its cpu_baseline to the line
+
+
 def _line(rt, metric, value, unit, args, config, extra):
     d = {"metric": metric, "value": value, "unit": unit, "n_gpus": rt.nranks,
          "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
          "scaling": "weak", "vs_baseline": None, "data": "synthetic", "config": config}
     d.update(extra)
+    if _LINE_HOOK is not None:
+        _LINE_HOOK(d)
     print(json.dumps(d), flush=True)
 
 
@@ -295,6 +300,10 @@ def _p2p_cli(args):
                                      transfer=TransferKind.D2D, allocation="asymmetric"))
         out[kind.value + "_asym"] = [(r.size_bytes, round(r.mean_us, 3),
                                       round(r.size_bytes / r.mean_us / 1e3, 2)) for r in rows]
+    # end to end: the same puts with a HOST payload (TransferKind.H2D, the
+    # reference's default kind) -- the PCIe leg is inside every timed put
+    e2e_rows = run_p2p(rt, BenchSpec(BenchKind.Bandwidth, (64 * MIB, 1 << 30), iters=3,
+                                     warmup=1))
     if rt.rank == 0:
         big = [gbps for n, _, gbps in out["bw"] if n >= 64 * MIB]
         value = out["bw"][-1][2]
@@ -313,7 +322,13 @@ def _p2p_cli(args):
                                                          if n >= 64 * MIB),
                               "put_latency_us_8B": out["put_asym"][0][1],
                               "get_latency_us_8B": out["get_asym"][0][1]},
-               "rows": out, "row_format": "[bytes, mean_us, GB/s]"})
+               "rows": out, "row_format": "[bytes, mean_us, GB/s]",
+               "e2e": {"value": round(e2e_rows[-1].size_bytes / e2e_rows[-1].mean_us / 1e3, 2),
+                       "unit": "GB/s", "h2d_bytes_per_step": e2e_rows[-1].size_bytes,
+                       "d2h_bytes_per_step": 0,
+                       "rows": [(r.size_bytes, round(r.size_bytes / r.mean_us / 1e3, 2))
+                                for r in e2e_rows],
+                       "note": "1 GiB puts from a host buffer (TransferKind.H2D) to rank 1"}})
     rt.finalize()
     return 0
 
@@ -343,6 +358,7 @@ def _coll_cli(args, kind):
                     os.environ.pop("DIOMP_ALLREDUCE_ALGO", None)
                 else:
                     os.environ["DIOMP_ALLREDUCE_ALGO"] = prev
+    e2e = _coll_e2e(rt, kind, 1 << 30)
     if rt.rank == 0:
         k = rt.nranks
         factor = 2 * (k - 1) / k if kind == "allreduce" else 1.0
@@ -357,6 +373,12 @@ def _coll_cli(args, kind):
                  "rows": table, "row_format": "[bytes, mean_us, busBW GB/s]",
                  "algorithm": "exact (reference ring-fold order, bitwise)" if kind == "allreduce"
                  else "p2p"}
+        extra["e2e"] = {"value": round(factor * e2e["bytes"] / e2e["seconds"] / 1e9, 2),
+                        "unit": "GB/s (busBW)", "h2d_bytes_per_step": e2e["bytes"],
+                        "d2h_bytes_per_step": e2e["bytes"], "seconds": round(e2e["seconds"], 5),
+                        "note": "host buffer -> put (H2D) into the own send buffer, the "
+                                "collective, get (D2H) of the result, on every rank; "
+                                "wall clock, max over ranks"}
         if nvls_rows:
             nt = tab(nvls_rows)
             extra["nvls"] = {"busbw_1GiB": nt[-1][2], "rows": nt,
@@ -366,6 +388,33 @@ def _coll_cli(args, kind):
               {"workload": f"{kind}_f32_sum_sweep_1KiB_1GiB", "endpoints": k}, extra)
     rt.finalize()
     return 0
+
+
+def _coll_e2e(rt, kind: str, nbytes: int, reps: int = 3) -> dict:
+    """One collective end to end through the public API with host buffers."""
+    comm = coll.bootstrap(rt, rt.world)
+    send = rt.alloc_symmetric(nbytes, 0)
+    recv = rt.alloc_symmetric(nbytes, 0)
+    host = np.random.default_rng(2000 + rt.rank).uniform(-1, 1, nbytes // 4).astype(np.float32)
+    out = np.empty_like(host)
+    op = coll.ReduceOp(coll.ReduceKind.Sum, coll.ElementType.f32)
+    me = GlobalAddress(rt.rank, 0, send.addr.offset)
+    res = GlobalAddress(rt.rank, 0, (recv if kind == "allreduce" else send).addr.offset)
+    best = float("inf")
+    for _ in range(reps):
+        rt.barrier(rt.world)
+        t0 = time.perf_counter()
+        rt.put(me, host, nbytes, TransferKind.H2D)
+        rt.fence(rt.world)
+        if kind == "allreduce":
+            coll.allreduce(comm, send.addr, recv.addr, nbytes // 4, op)
+        else:
+            coll.bcast(comm, send.addr, nbytes, root=0)
+        rt.get(res, out, nbytes, TransferKind.D2H).wait(rt.cfg.timeout)
+        best = min(best, time.perf_counter() - t0)
+    rt.free(recv)
+    rt.free(send)
+    return {"bytes": nbytes, "seconds": _max_over_ranks(rt, f"e2e/{kind}", best)}
 
 
 def _dgemm_cli(args):

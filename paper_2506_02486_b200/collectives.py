@@ -282,6 +282,9 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
     algo = algorithm or os.environ.get("DIOMP_ALLREDUCE_ALGO", "exact")
     if algo not in ("exact", "nvls"):
         raise UsageError(f"unknown allreduce algorithm {algo!r}")
+    if algo == "nvls" and not _native.has_experiments():
+        raise UsageError("allreduce algorithm 'nvls' is in the experiments build only "
+                         "(python paper_2506_02486_b200/build.py -DDIOMP_EXPERIMENTS)")
     if k == 1:
         ep = comm.ring[0]
         if send.offset != recv.offset:

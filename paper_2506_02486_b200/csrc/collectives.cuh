@@ -226,15 +226,20 @@ __global__ void __launch_bounds__(THREADS) reduce_kernel(const __grid_constant__
     } else if (a.mode == 1) {
         fold_range<T, OP, KMAX>(a, lo, hi, a.root, a.root);
         exit_barrier(a.t, 2);
-    } else {
+    }
+#ifdef DIOMP_EXPERIMENTS
+    else {
         fold_range<T, OP, KMAX>(a, lo, hi, p, p);
     }
+#endif
 }
 
+#ifdef DIOMP_EXPERIMENTS
 // Allreduce step 3 of 3 (after the copy-engine pushes of step 2): signal
 // every peer epoch+3 and wait for theirs -- our block has landed in every
 // member's recv and theirs in ours.
 __global__ void allreduce_exit_kernel(const __grid_constant__ Args a) { exit_barrier(a.t, 3); }
+#endif
 
 // bcast: non-root position p handles block j = (p - root - 1 mod k) of k-1.
 template <int U>
@@ -288,6 +293,10 @@ __global__ void __launch_bounds__(THREADS) bcast_kernel(const __grid_constant__ 
     exit_barrier(a.t);
 }
 
+#ifdef DIOMP_EXPERIMENTS
+// Experiments build only (-DDIOMP_EXPERIMENTS): measured slower than the
+// default pull+push bcast on 4 B200 (profiles/r01_bcast_chain_sweep.txt,
+// profiles/r01_bcast_pullchain_sweep.txt), kept out of the product library.
 // bcast, chain algorithm (k >= 3, large buffers): positions in ring order
 // from the root form a pipeline root -> root+1 -> ... -> root+k-1.  The body
 // (16-B vectors) is cut into chunks; CTA b of every position handles chunks
@@ -464,6 +473,8 @@ static bool bcast_pullchain() {
     return v == 1;
 }
 
+#endif  // DIOMP_EXPERIMENTS
+
 // CTAs per SM (512 threads each).  Measured through the C ABI
 // (tools/coll_probe.cpp, profiles/r01_collprobe_k{2,4}.txt): 2 CTAs/SM wins
 // below 256 MiB (16 MiB allreduce k=2: 399 vs 324 GB/s busBW; 64 MiB k=4:
@@ -486,6 +497,7 @@ static int grid_for(uint64_t work_items, int per_sm) {
     return (int)want;
 }
 
+#ifdef DIOMP_EXPERIMENTS
 // Allreduce algorithm.  fused (default): one kernel, block p folded from the
 // peers' send buffers (loads) and stored to every member (SM stores).  ce: the
 // same fold into the own recv only, then the copy engine pushes block p to
@@ -506,13 +518,17 @@ static uint64_t ar_ce_min() {
     return g_ar_ce_min.load(std::memory_order_relaxed);
 }
 
+#endif  // DIOMP_EXPERIMENTS
+
 template <typename T, typename OP>
 static int launch_reduce(Args a, cudaStream_t s) {
     const uint64_t per = a.count / a.t.k + 1;
     const uint64_t items = per / (16 / sizeof(T)) + 1;
     const int g = grid_for(items, ctas_per_sm(a.count * sizeof(T), true));
+#ifdef DIOMP_EXPERIMENTS
     const bool ce = a.mode == 0 && a.t.sync && a.t.k > 1 && a.count * sizeof(T) >= ar_ce_min();
     if (ce) a.mode = 2;
+#endif
     // KMAX = smallest supported team bound >= k (register footprint, and the
     // per-thread unroll, follow the actual team size)
     if (a.t.k <= 2) reduce_kernel<T, OP, 2><<<g, THREADS, 0, s>>>(a);
@@ -521,6 +537,7 @@ static int launch_reduce(Args a, cudaStream_t s) {
     else if (a.t.k <= 16) reduce_kernel<T, OP, 16><<<g, THREADS, 0, s>>>(a);
     else reduce_kernel<T, OP, DIOMP_MAX_TEAM><<<g, THREADS, 0, s>>>(a);
     DIOMP_LAUNCH_CHECK();
+#ifdef DIOMP_EXPERIMENTS
     if (ce) {
         const int k = a.t.k, p = a.t.pos;
         const uint64_t lo = (uint64_t)p * a.count / k * sizeof(T);
@@ -536,6 +553,7 @@ static int launch_reduce(Args a, cudaStream_t s) {
         allreduce_exit_kernel<<<1, 64, 0, s>>>(a);
         DIOMP_LAUNCH_CHECK();
     }
+#endif
     return DIOMP_OK;
 }
 
@@ -568,6 +586,7 @@ static bool team_ok(const diomp_team *t) {
 
 extern "C" {
 
+#ifdef DIOMP_EXPERIMENTS
 int diomp_set_allreduce_ce_min(uint64_t bytes) {
     diomp::coll::ar_ce_min();  // settle the environment default first
     diomp::coll::g_ar_ce_min.store(bytes, std::memory_order_relaxed);
@@ -584,6 +603,7 @@ int diomp_set_bcast_pullchain(int32_t on) {
     diomp::coll::g_bcast_pullchain.store(on ? 1 : 0, std::memory_order_relaxed);
     return DIOMP_OK;
 }
+#endif  // DIOMP_EXPERIMENTS
 
 int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, uint64_t count,
                     int32_t dtype, int32_t op, void *stream) {
@@ -628,6 +648,7 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
     a.recv_off = offset;
     a.count = nbytes;
     a.root = root;
+#ifdef DIOMP_EXPERIMENTS
     if (team->sync && team->k >= 3 && nbytes >= bcast_chain_min() && nbytes >= 16 * CHAIN_GMAX) {
         // chunk / CTA count: DIOMP_BCAST_CHAIN_CHUNK (bytes), DIOMP_BCAST_CHAIN_G
         static const uint64_t env_chunk = [] {
@@ -648,6 +669,7 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
         DIOMP_LAUNCH_CHECK();
         return DIOMP_OK;
     }
+#endif
     const uint64_t per = nbytes / (uint64_t)(team->k - 1) / 16 + 1;
     const int g = grid_for(per, ctas_per_sm(nbytes, false));
     // 16-B vectors in flight per thread (DIOMP_BCAST_U = 2 | 4 | 8 overrides).

@@ -450,22 +450,35 @@ int diomp_copy(int device, uint64_t dst, uint64_t src, uint64_t nbytes, void *st
 // kernel from 16 MiB (785 GB/s at 1 GiB) and through the SM loop below that.
 // Small transfers stay on the SM kernel (lowest issue latency).
 // DIOMP_PUT_ENGINE = auto|sm|ce, DIOMP_GET_ENGINE = auto|sm|tma.
-static uint64_t g_put_ce_min = ~0ull, g_get_bulk_min = ~0ull;
+// Small transfers (tools/lat_probe.cu on 2 B200, 8 B peer copy, host issue +
+// event wait): copy engine 8.55 us (1.3 us to issue) vs 10.7 us (2.6 us) for
+// a one-thread SM kernel -- an empty kernel alone is 8.7 us -- so remote
+// puts of any size go to the copy engine.  Small remote gets measured the
+// other way through the Python API (8 B get+wait 15.3 us on the copy engine
+// vs 14.2 on the SM kernel), so they stay on the kernel
+// (DIOMP_GET_ENGINE=ce: copy engine up to 64 KiB).
+static uint64_t g_put_ce_min = ~0ull, g_get_bulk_min = ~0ull, g_get_ce_max = 0;
 static std::once_flag g_engine_once;
 
 static void init_engines() {
     std::call_once(g_engine_once, [] {
         const char *pe = getenv("DIOMP_PUT_ENGINE");
         const char *ge = getenv("DIOMP_GET_ENGINE");
-        g_put_ce_min = (pe && !strcmp(pe, "sm")) ? ~0ull : (pe && !strcmp(pe, "ce")) ? 1 : (64ull << 10);
+        g_put_ce_min = (pe && !strcmp(pe, "sm")) ? ~0ull : 1;
         g_get_bulk_min = (ge && !strcmp(ge, "sm")) ? ~0ull : (ge && !strcmp(ge, "tma")) ? 16 : (16ull << 20);
+        g_get_ce_max = (ge && !strcmp(ge, "ce")) ? (64ull << 10) : 0;
     });
+}
+
+static inline int current_device_is(int device) {
+    int cur = -1;
+    return cudaGetDevice(&cur) == cudaSuccess && cur == device;
 }
 
 int diomp_put(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int remote, void *stream) {
     if (nbytes == 0) return DIOMP_OK;
     init_engines();
-    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    if (!current_device_is(device)) DIOMP_CUDA_TRY(cudaSetDevice(device));
     if (remote && nbytes >= g_put_ce_min) {
         DIOMP_CUDA_TRY(cudaMemcpyAsync((void *)dst, (const void *)src, nbytes,
                                        cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
@@ -477,8 +490,13 @@ int diomp_put(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int remot
 int diomp_get(int device, uint64_t dst, uint64_t src, uint64_t nbytes, int remote, void *stream) {
     if (nbytes == 0) return DIOMP_OK;
     init_engines();
-    DIOMP_CUDA_TRY(cudaSetDevice(device));
+    if (!current_device_is(device)) DIOMP_CUDA_TRY(cudaSetDevice(device));
     cudaStream_t s = (cudaStream_t)stream;
+    if (remote && nbytes <= g_get_ce_max) {
+        DIOMP_CUDA_TRY(cudaMemcpyAsync((void *)dst, (const void *)src, nbytes,
+                                       cudaMemcpyDeviceToDevice, s));
+        return DIOMP_OK;
+    }
     if (remote && nbytes >= g_get_bulk_min && ((dst ^ src) & 15) == 0) {
         uint64_t head = (16 - (dst & 15)) & 15;
         uint64_t body = (nbytes - head) / 16 * 16;

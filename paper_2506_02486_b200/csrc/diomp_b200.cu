@@ -5,8 +5,13 @@
 
 #include "common.cuh"
 #include "core.cuh"
+#include "rma.cuh"
 #include "heap.cuh"
 #include "stencil.cuh"
 #include "collectives.cuh"
 #include "gemm.cuh"
+#ifdef DIOMP_EXPERIMENTS
+// NVSwitch multicast allreduce: measured slower than the exact P2P kernel on
+// this box, experiments build only
 #include "nvls.cuh"
+#endif

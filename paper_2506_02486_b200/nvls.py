@@ -27,6 +27,8 @@ DEFAULT_WINDOW = 256 << 20
 
 
 def supported(gpu: int) -> bool:
+    if not _native.has_experiments():   # NVLS lives in the experiments build only
+        return False
     v = _native.ctypes.c_int(0)
     _native.call("diomp_mc_supported", gpu, _native.ctypes.byref(v))
     return bool(v.value)

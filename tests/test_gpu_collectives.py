@@ -146,7 +146,13 @@ def test_device_flag_mode_back_to_back():
         assert all(r[rep] == want for r in res)
 
 
+_EXPERIMENTS = pytest.mark.skipif(
+    not __import__("paper_2506_02486_b200._native", fromlist=["x"]).has_experiments(),
+    reason="experiments build only (-DDIOMP_EXPERIMENTS)")
+
+
 @need_gpus(3)
+@_EXPERIMENTS
 @pytest.mark.parametrize("pull", [0, 1])
 def test_bcast_chain_device_flags(pull):
     """Chain bcast (k >= 3, per-CTA progress flags), push and pull flavours:
@@ -193,7 +199,7 @@ def test_bcast_chain_device_flags(pull):
 
 
 @need_gpus(2)
-@pytest.mark.parametrize("ce_min", [None, 8 * MIB])
+@pytest.mark.parametrize("ce_min", [None, pytest.param(8 * MIB, marks=_EXPERIMENTS)])
 def test_allreduce_device_flag_algorithms_bitwise(ce_min):
     """Device-flag rings, both allreduce algorithms (fused; fold + copy-engine
     push from ce_min bytes): bitwise equal to the reference fold order, odd
@@ -237,7 +243,8 @@ def test_allreduce_device_flag_algorithms_bitwise(ce_min):
     try:
         res = run_emulated(k, fn, segment_bytes=256 * MIB)
     finally:
-        _native.call("diomp_set_allreduce_ce_min", (1 << 64) - 1)
+        if ce_min is not None:
+            _native.call("diomp_set_allreduce_ce_min", (1 << 64) - 1)
     j = 0
     for i, (et, kind, count, delta) in enumerate(cases):
         want = O.allreduce_fold([contrib(r, et, count, i) for r in range(k)], kind).tobytes()
@@ -247,6 +254,7 @@ def test_allreduce_device_flag_algorithms_bitwise(ce_min):
 
 
 @need_gpus(2)
+@_EXPERIMENTS
 def test_allreduce_nvls_in_switch(monkeypatch):
     """NVSwitch multicast allreduce (algorithm="nvls"): integer sum/min/max
     bitwise equal to the reference fold, float sums within the north-star

@@ -15,6 +15,8 @@ LIB = os.path.join(ROOT, "paper_2506_02486_b200", "libdiomp_b200.so")
 def _declared():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    # the experiments block is not part of the product library
+    text = re.sub(r"#ifdef DIOMP_EXPERIMENTS.*?#endif", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(diomp_[a-z0-9_]+)\s*\(", text)))
 
 

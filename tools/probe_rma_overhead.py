@@ -1,5 +1,5 @@
 """Host-side cost of one put/get (D2D, 8 B) through the public API:
-2 thread-ranks on GPU 0, rank 0 issues N puts back to back, then fences.
+2 thread-ranks (GPUs 0 and 1 when present), rank 0 issues N puts back to back, then fences.
 Prints us/op and a cProfile of the put loop."""
 import cProfile
 import os
@@ -52,4 +52,6 @@ def fn(rt):
     return out
 
 
-print(run_emulated(2, fn, segment_bytes=8 << 20)[0])
+import torch
+print(run_emulated(2, fn, segment_bytes=8 << 20,
+                   gpus=[0, 1] if torch.cuda.device_count() >= 2 else [0])[0])
