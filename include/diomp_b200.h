@@ -158,9 +158,13 @@ int diomp_wait(int device, uint64_t flag_addr, uint64_t value, void *stream);
  * from `device`; flags of endpoint p live at base[p] + flag_off, slot index =
  * slot[q] (the global endpoint index of the signalling position q).
  * epoch_to[q] / epoch_from[q]: signals already sent to / received from q on
- * this pair; an entry+exit synchronised call consumes two (+1 entry, +2 exit)
- * and the caller advances both by 2 afterwards -- allreduce consumes three
- * (+1 entry, +2 phase, +3 exit) on both of its algorithms.  sync=0 skips all flag
+ * this pair.  Every collective call consumes ONE signal per pair -- its entry
+ * handshake (block 0 signals +1 at kernel start, every CTA waits for the
+ * peers' +1) -- and the caller advances both epochs by 1.  There is no exit
+ * handshake inside the kernels: the next call's entry certifies the previous
+ * one's completion toward each peer (the peer's stream has moved past it).
+ * Where the caller itself needs the result, diomp_team_barrier behind the
+ * kernel is the exit (one more signal, +1 again).  sync=0 skips all flag
  * traffic (the caller orders the endpoints with host barriers; used when
  * several endpoints share one GPU).                                           */
 typedef struct {

@@ -209,10 +209,14 @@ def run_collective(rt: Runtime, spec: BenchSpec, comm=None) -> list[BenchRow]:
             run_once(size, True)
         rt.barrier(rt.world)
         if device_timed:
-            # enqueue-only repetitions, CUDA events on the RMA stream (device time)
+            # enqueue-only repetitions, CUDA events on the RMA stream (device
+            # time); a device-side team barrier first, so the timed region
+            # starts with every GPU in step (host barrier skew excluded)
+            coll._exit(comm)
             timer.start()
             for _ in range(spec.iters):
                 run_once(size, False)
+            coll._exit(comm)   # the last call's results in place, inside the timed region
             elapsed = timer.stop_ms() / 1e3
             _native.check_device(rt.gpus[0], "collective bench")
         else:

@@ -12,7 +12,9 @@ the reference's combination orders reproduced bit for bit:
                at ring position b, and every member ends with all blocks.
 
 Synchronisation: when every endpoint of the ring is on its own GPU the kernels
-meet on system-scope flags (entry and exit) -- no host round trip.  When
+meet on system-scope flags -- an entry handshake per call, an exit handshake
+only where the caller needs the result (blocking calls, complete()) -- no
+host round trip.  When
 endpoints share a GPU (the in-process emulation on a small box) the host
 orders them with control-plane barriers instead, because kernels that spin on
 each other must never share a GPU.
@@ -47,11 +49,16 @@ class ElementType(enum.Enum):
 
     @property
     def dtype(self) -> np.dtype:
-        return np.dtype({"f32": "<f4", "f64": "<f8", "i32": "<i4", "i64": "<i8"}[self.value])
+        return _ET_DTYPE[self.value]
 
     @property
     def code(self) -> int:
-        return {"f32": 0, "f64": 1, "i32": 2, "i64": 3}[self.value]
+        return _ET_CODE[self.value]
+
+
+_ET_DTYPE = {k: np.dtype(v) for k, v in
+             {"f32": "<f4", "f64": "<f8", "i32": "<i4", "i64": "<i8"}.items()}
+_ET_CODE = {"f32": 0, "f64": 1, "i32": 2, "i64": 3}
 
 
 @dataclass(frozen=True)
@@ -66,7 +73,10 @@ class ReduceOp:
 
     @property
     def code(self) -> int:
-        return {ReduceKind.Sum: 0, ReduceKind.Min: 1, ReduceKind.Max: 2}[self.kind]
+        return _RK_CODE[self.kind.value]
+
+
+_RK_CODE = {"sum": 0, "min": 1, "max": 2}
 
 
 class UniqueId:
@@ -157,27 +167,83 @@ def _team(comm: Communicator, pos: int, sync: int) -> _native.Team:
     return t
 
 
+_torch_ev: dict = {}
+
+
 def _after_torch(rt: Runtime, device: int):
-    """Order our stream after pending torch work on the same GPU (arena writes
-    made through torch run on torch's current stream)."""
-    import torch
+    """Order our RMA stream after pending torch work on the same GPU (arena
+    writes made through torch run on torch's current stream): an event on
+    torch's stream and a stream wait -- no host synchronisation."""
     gpu = rt.gpus[device]
-    torch.cuda.current_stream(gpu).synchronize()
+    ev = _torch_ev.get(gpu)
+    if ev is None:
+        ev = _torch_ev[gpu] = _native.event_create(gpu, timing=False)
+    rc = _native.lib.diomp_event_record(ev, _torch_stream(gpu))
+    if not rc:
+        rc = _native.lib.diomp_stream_wait_event(rt._rma_streams[device].handle, ev)
+    if rc:
+        _native.check(rc, "order after torch")
 
 
-def _run(comm: Communicator, launch, blocking: bool = True, signals: int = 2):
+def _torch_stream(gpu: int) -> int:
+    import torch
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    return raw(gpu) if raw is not None else torch.cuda.current_stream(gpu).cuda_stream
+
+
+def _advance(comm: Communicator, n: int):
+    rt = comm.rt
+    for pos in comm.my_positions:
+        me_ep = comm.ring[pos]
+        me = rt.endpoint_index(me_ep.rank, me_ep.device)
+        for q, ep in enumerate(comm.ring):
+            if q != pos:
+                rt.advance_pair(me, rt.endpoint_index(ep.rank, ep.device), n, CHANNEL_COLL)
+
+
+def _exit(comm: Communicator):
+    """The exit handshake of the calls enqueued so far: every local position
+    signals its peers and waits for theirs (one-CTA diomp_team_barrier behind
+    the collective kernels on the RMA stream).  Afterwards every member's
+    stores into this position's buffers have landed."""
+    rt = comm.rt
+    for pos in comm.my_positions:
+        ep = comm.ring[pos]
+        _native.check(_native.lib.diomp_team_barrier(_team(comm, pos, 1),
+                                                     rt._rma_streams[ep.device].handle),
+                      "collective exit")
+    _advance(comm, 1)
+    comm._pending = False
+
+
+def complete(comm: Communicator):
+    """Collective over the communicator: results of every blocking=False call
+    issued on it so far are in place (the reference's calls are blocking; this
+    is the completion point of the non-blocking form)."""
+    rt = comm.rt
+    if comm.device_sync and comm.size > 1 and comm.__dict__.get("_pending"):
+        _exit(comm)
+    for pos in comm.my_positions:
+        s = rt._rma_streams[comm.ring[pos].device]
+        s.synchronize()
+        _native.check_device(s.gpu, "collective")
+
+
+def _run(comm: Communicator, launch, blocking: bool = True):
     """launch(team, stream) for every local position, device- or host-synchronised.
-    `signals` = device signals the call consumes per ordered pair (allreduce 3:
-    entry, phase, exit; reduce / bcast 2: entry, exit).
-    blocking=False (device-synchronised rings only) enqueues and returns: the
-    result is ready once the rank's RMA stream of that device has drained."""
+
+    Device-synchronised rings: every call costs one signal per ordered pair
+    (the kernel's entry handshake); a blocking call adds the exit handshake
+    (one more) and waits for it.  blocking=False enqueues and returns -- the
+    next call's entry handshake certifies this one's completion toward each
+    peer, and complete(comm) (or any blocking call) makes results visible.
+    Members must agree on `blocking` call by call, as on the call itself."""
     rt = comm.rt
     sync = 1 if (comm.device_sync and comm.size > 1) else 0
     if not sync:
         blocking = True
-    if blocking:
-        for pos in comm.my_positions:
-            _after_torch(rt, comm.ring[pos].device)
+    for pos in comm.my_positions:
+        _after_torch(rt, comm.ring[pos].device)
     if not sync and comm.size > 1:
         rt.barrier(comm.group)
     used = []
@@ -186,19 +252,16 @@ def _run(comm: Communicator, launch, blocking: bool = True, signals: int = 2):
         s = rt._rma_streams[ep.device]
         _native.check(launch(_team(comm, pos, sync), s.handle), "collective launch")
         used.append((pos, s))
+    if sync:
+        _advance(comm, 1)
+        comm._pending = True
+        if blocking:
+            _exit(comm)
     if blocking:
         for pos, s in used:
             s.synchronize()
             _native.check_device(s.gpu, "collective")
-    if sync:
-        for pos in comm.my_positions:
-            me_ep = comm.ring[pos]
-            me = rt.endpoint_index(me_ep.rank, me_ep.device)
-            for q, ep in enumerate(comm.ring):
-                if q != pos:
-                    rt.advance_pair(me, rt.endpoint_index(ep.rank, ep.device), signals,
-                                    CHANNEL_COLL)
-    elif comm.size > 1:
+    if not sync and comm.size > 1:
         rt.barrier(comm.group)
 
 
@@ -270,6 +333,15 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
     (multimem.ld_reduce) -- integer results identical, float sums within
     rounding (rel-L2 1e-6 f32 / 1e-12 f64), float min/max refused."""
     rt, k = comm.rt, comm.size
+    algo = algorithm or os.environ.get("DIOMP_ALLREDUCE_ALGO", "exact")
+    memo = comm.__dict__.setdefault("_memo", {})
+    key = ("allreduce", send, recv, count, op, algo)
+    if memo.get(key) == rt._ledger_gen and k > 1 and algo == "exact":
+        # same call shape validated since the last allocation change
+        comm._next_seq()
+        _run(comm, lambda t, s: _native.lib.diomp_allreduce(
+            t, send.offset, recv.offset, count, op.etype.code, op.code, s), blocking)
+        return
     _check_typed(send, count, op.etype)
     _check_typed(recv, count, op.etype)
     nbytes = count * op.etype.dtype.itemsize
@@ -279,7 +351,6 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
             rt.gm.check_rma_range(ep.device, recv.offset, max(nbytes, 1))
     if count == 0:
         return
-    algo = algorithm or os.environ.get("DIOMP_ALLREDUCE_ALGO", "exact")
     if algo not in ("exact", "nvls"):
         raise UsageError(f"unknown allreduce algorithm {algo!r}")
     if algo == "nvls" and not _native.has_experiments():
@@ -299,9 +370,9 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
     if algo == "nvls":
         _allreduce_nvls(comm, send, recv, count, op, blocking)
         return
+    memo[key] = rt._ledger_gen
     _run(comm, lambda t, s: _native.lib.diomp_allreduce(t, send.offset, recv.offset, count,
-                                                        op.etype.code, op.code, s), blocking,
-         signals=3)
+                                                        op.etype.code, op.code, s), blocking)
 
 
 def _allreduce_nvls(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, count: int,
@@ -339,4 +410,4 @@ def device_bcast(rt: Runtime, var: GlobalAddress, nbytes: int, group: Group):
 
 
 __all__ = ["ReduceKind", "ElementType", "ReduceOp", "UniqueId", "Communicator", "bootstrap",
-           "bcast", "reduce", "allreduce", "device_bcast", "InvalidAddress"]
+           "bcast", "reduce", "allreduce", "complete", "device_bcast", "InvalidAddress"]

@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -108,24 +109,18 @@ __device__ __forceinline__ void entry_barrier(const diomp_team &t) {
     __syncthreads();
 }
 
-// Exit: the last CTA signals epoch+`e` to every peer and waits for theirs.
-// Allreduce consumes three signals per call (entry, phase, exit) on both of
-// its paths, reduce and bcast two.
-__device__ __forceinline__ void exit_barrier(const diomp_team &t, int e = 2) {
-    if (!t.sync) return;
-    if (last_cta_done((unsigned int *)(t.base[t.pos] + t.counter_off), gridDim.x)) {
-        const int q = threadIdx.x;
-        if (q < t.k && q != t.pos) {
-            st_release_sys((uint64_t *)(t.base[q] + t.flag_off) + t.slot[t.pos], t.epoch_to[q] + e);
-            wait_ge((const uint64_t *)(t.base[t.pos] + t.flag_off) + t.slot[q], t.epoch_from[q] + e);
-        }
-    }
-}
+// There is no exit handshake inside the collective kernels.  A call is
+// complete toward a peer once that peer's stream has moved past it, which the
+// next collective's entry signal (raised by block 0 at kernel start, after
+// the previous kernel has retired) certifies -- so back-to-back collectives
+// pay one handshake each, not two.  When the caller needs the result itself
+// (a blocking call, coll.complete()), a one-CTA diomp_team_barrier after the
+// kernel is the exit.
 
 // Fold element range [lo, hi) of T over positions start, start+1, ... (mod k)
 // and store to the recv buffer of every position in [dst_lo, dst_hi) (all) or
 // to `only` (reduce).  Vectorised 16 B where the offsets allow.
-template <typename T, typename OP, int KMAX>
+template <typename T, typename OP, int KMAX, int U = (KMAX <= 4 ? 2 : 1)>
 __device__ __forceinline__ void fold_range(const Args &a, uint64_t lo, uint64_t hi, int start,
                                            int only) {
     const diomp_team &t = a.t;
@@ -152,7 +147,6 @@ __device__ __forceinline__ void fold_range(const Args &a, uint64_t lo, uint64_t 
     // U independent vectors per thread per iteration: all k*U loads are in
     // flight before the first fold (NVLink load latency ~2 us needs MBs in
     // flight per GPU)
-    constexpr int U = KMAX <= 4 ? 2 : 1;
     for (uint64_t v0 = gtid; v0 < nvec; v0 += gsz * U) {
         VT buf[U][KMAX];
 #pragma unroll
@@ -215,31 +209,23 @@ __device__ __forceinline__ void fold_range(const Args &a, uint64_t lo, uint64_t 
 // mode 1: reduce to the root;
 // mode 2: allreduce step 1 of 3 (fold block p into the own recv only; the
 //         copy engine then pushes it to every peer).
-template <typename T, typename OP, int KMAX>
+template <typename T, typename OP, int KMAX, int U = (KMAX <= 4 ? 2 : 1)>
 __global__ void __launch_bounds__(THREADS) reduce_kernel(const __grid_constant__ Args a) {
     entry_barrier(a.t);
     const int k = a.t.k, p = a.t.pos;
     const uint64_t lo = (uint64_t)p * a.count / k, hi = (uint64_t)(p + 1) * a.count / k;
     if (a.mode == 0) {
-        fold_range<T, OP, KMAX>(a, lo, hi, p, -1);
-        exit_barrier(a.t, 3);
+        fold_range<T, OP, KMAX, U>(a, lo, hi, p, -1);
     } else if (a.mode == 1) {
-        fold_range<T, OP, KMAX>(a, lo, hi, a.root, a.root);
-        exit_barrier(a.t, 2);
+        fold_range<T, OP, KMAX, U>(a, lo, hi, a.root, a.root);
     }
 #ifdef DIOMP_EXPERIMENTS
     else {
-        fold_range<T, OP, KMAX>(a, lo, hi, p, p);
+        fold_range<T, OP, KMAX, U>(a, lo, hi, p, p);
     }
 #endif
 }
 
-#ifdef DIOMP_EXPERIMENTS
-// Allreduce step 3 of 3 (after the copy-engine pushes of step 2): signal
-// every peer epoch+3 and wait for theirs -- our block has landed in every
-// member's recv and theirs in ours.
-__global__ void allreduce_exit_kernel(const __grid_constant__ Args a) { exit_barrier(a.t, 3); }
-#endif
 
 // bcast: non-root position p handles block j = (p - root - 1 mod k) of k-1.
 template <int U>
@@ -290,7 +276,6 @@ __global__ void __launch_bounds__(THREADS) bcast_kernel(const __grid_constant__ 
             }
         }
     }
-    exit_barrier(a.t);
 }
 
 #ifdef DIOMP_EXPERIMENTS
@@ -376,7 +361,6 @@ __global__ void __launch_bounds__(THREADS) bcast_chain_kernel(const __grid_const
                 if (q != root) reinterpret_cast<uint8_t *>(t.base[q] + off)[e] = b;
         }
     }
-    exit_barrier(a.t);
 }
 
 // bcast, pull chain: the same root -> root+1 -> ... pipeline, but every hop
@@ -438,7 +422,6 @@ __global__ void __launch_bounds__(THREADS) bcast_pullchain_kernel(const __grid_c
                 if (q != root) reinterpret_cast<uint8_t *>(t.base[q] + off)[e] = b;
         }
     }
-    exit_barrier(a.t);
 }
 
 // bcast algorithm: chain for k >= 3 from DIOMP_BCAST_CHAIN_MIN bytes (default
@@ -487,7 +470,10 @@ static int ctas_per_sm(uint64_t bytes, bool reduce) {
         return x < 0 ? 0 : (x > 4 ? 4 : x);
     }();
     if (env) return env;
-    return (reduce && bytes >= (256ull << 20)) ? 4 : 2;
+    // round 2 sweep (profiles/r02_coll_sweep.txt, 4 B200, no exit handshake):
+    // 4 CTAs/SM from 64 MiB for the reduction kernels (k=2 64 MiB 610 -> 617,
+    // k=4 628 -> 633 GB/s busBW)
+    return (reduce && bytes >= (64ull << 20)) ? 4 : 2;
 }
 
 static int grid_for(uint64_t work_items, int per_sm) {
@@ -531,7 +517,20 @@ static int launch_reduce(Args a, cudaStream_t s) {
 #endif
     // KMAX = smallest supported team bound >= k (register footprint, and the
     // per-thread unroll, follow the actual team size)
-    if (a.t.k <= 2) reduce_kernel<T, OP, 2><<<g, THREADS, 0, s>>>(a);
+    // vectors in flight per thread per source (DIOMP_COLL_U = 1 | 2 | 4 for
+    // f32 sums, the benchmarked op; default 2 for k <= 4)
+    static const int env_u = [] {
+        const char *e = getenv("DIOMP_COLL_U");
+        return e ? atoi(e) : 0;
+    }();
+    constexpr bool probe = std::is_same<T, float>::value && std::is_same<OP, Sum<float>>::value;
+    if (probe && env_u == 1 && a.t.k <= 4) {
+        if (a.t.k <= 2) reduce_kernel<T, OP, 2, 1><<<g, THREADS, 0, s>>>(a);
+        else reduce_kernel<T, OP, 4, 1><<<g, THREADS, 0, s>>>(a);
+    } else if (probe && env_u == 4 && a.t.k <= 4) {
+        if (a.t.k <= 2) reduce_kernel<T, OP, 2, 4><<<g, THREADS, 0, s>>>(a);
+        else reduce_kernel<T, OP, 4, 4><<<g, THREADS, 0, s>>>(a);
+    } else if (a.t.k <= 2) reduce_kernel<T, OP, 2><<<g, THREADS, 0, s>>>(a);
     else if (a.t.k <= 4) reduce_kernel<T, OP, 4><<<g, THREADS, 0, s>>>(a);
     else if (a.t.k <= 8) reduce_kernel<T, OP, 8><<<g, THREADS, 0, s>>>(a);
     else if (a.t.k <= 16) reduce_kernel<T, OP, 16><<<g, THREADS, 0, s>>>(a);
@@ -550,8 +549,6 @@ static int launch_reduce(Args a, cudaStream_t s) {
                 DIOMP_CUDA_TRY(cudaMemcpyAsync(dst, src, hi - lo, cudaMemcpyDeviceToDevice, s));
             }
         }
-        allreduce_exit_kernel<<<1, 64, 0, s>>>(a);
-        DIOMP_LAUNCH_CHECK();
     }
 #endif
     return DIOMP_OK;
@@ -671,7 +668,14 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
     }
 #endif
     const uint64_t per = nbytes / (uint64_t)(team->k - 1) / 16 + 1;
-    const int g = grid_for(per, ctas_per_sm(nbytes, false));
+    // k >= 4 (profiles/r02_coll_sweep.txt): 1 CTA/SM with 2 vectors in flight
+    // between 32 and 256 MiB (64 MiB 610 -> 625 GB/s), 4 CTAs/SM with 4
+    // vectors from 256 MiB (1 GiB 617 -> 633)
+    int per_sm = ctas_per_sm(nbytes, false);
+    const bool big4 = team->k >= 4 && nbytes >= (256ull << 20);
+    const bool mid4 = team->k >= 4 && nbytes >= (32ull << 20) && !big4;
+    if (!getenv("DIOMP_COLL_CTAS_PER_SM")) per_sm = big4 ? 4 : mid4 ? 1 : per_sm;
+    const int g = grid_for(per, per_sm);
     // 16-B vectors in flight per thread (DIOMP_BCAST_U = 2 | 4 | 8 overrides).
     // Measured on 4 B200 (profiles/r01_bcast_u_sweep.txt): 2 beats 4 and 8 at
     // 2 CTAs/SM from 32 MiB -- fewer outstanding NVLink loads per SM, less
@@ -681,7 +685,7 @@ int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_
         const char *e = getenv("DIOMP_BCAST_U");
         return e ? atoi(e) : 0;
     }();
-    const int u = env_u ? env_u : (team->k >= 4 && nbytes < (32ull << 20) ? 4 : 2);
+    const int u = env_u ? env_u : (team->k >= 4 && (nbytes < (32ull << 20) || big4) ? 4 : 2);
     if (u == 4) bcast_kernel<4><<<g, THREADS, 0, (cudaStream_t)stream>>>(a);
     else if (u == 8) bcast_kernel<8><<<g, THREADS, 0, (cudaStream_t)stream>>>(a);
     else bcast_kernel<2><<<g, THREADS, 0, (cudaStream_t)stream>>>(a);

@@ -59,13 +59,13 @@ def test_interleaved_allreduce_stencil_ring_100_iterations():
             runner.enqueue(1, stream_handle=side)
             ring.enqueue_step()
             if it % 10 == 9:
-                rt._rma_streams[0].synchronize()
+                coll.complete(comm)
                 got = np.frombuffer(bytes(rt.gm.view(0, recv.addr.offset, count * 4)),
                                     dtype=np.float32)
                 ar_ok = ar_ok and got.tobytes() == want_ar.tobytes()
         _native.call("diomp_stream_sync", side)
         ring.synchronize()
-        rt._rma_streams[0].synchronize()
+        coll.complete(comm)
         _native.check_device(rt.gpus[0], "interleaved")
         rt.barrier(rt.world)
         f = _gather_field(rt, runner.cur_rec, runner.spec, runner.nxl, runner.shape)

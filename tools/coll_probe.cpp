@@ -46,7 +46,7 @@ int main(int argc, char **argv) {
         t.flag_off = FLAG; t.counter_off = CNT;
         for (int q = 0; q < K; ++q) { t.base[q] = base[q]; t.slot[q] = q; }
     }
-    const int per = ar ? 3 : 2;
+    const int per = 1;   // one entry handshake per call; the exit is a team barrier
     std::vector<uint64_t> sizes;
     for (uint64_t s = 1 << 20; s <= NMAX; s <<= 2) sizes.push_back(s);
     std::barrier bar(K);
@@ -62,13 +62,20 @@ int main(int argc, char **argv) {
             else CK(diomp_bcast(&t, SEND, bytes, 0, st[p]));
             for (int q = 0; q < K; ++q) if (q != p) { t.epoch_to[q] += per; t.epoch_from[q] += per; }
         };
+        auto exit_barrier = [&]() {
+            if (!t.sync) return;
+            CK(diomp_team_barrier(&t, st[p]));
+            for (int q = 0; q < K; ++q) if (q != p) { t.epoch_to[q] += 1; t.epoch_from[q] += 1; }
+        };
         for (uint64_t bytes : sizes) {
             const int iters = bytes >= (256ull << 20) ? 10 : 50;
             for (int w = 0; w < 3; ++w) once(bytes);
+            exit_barrier();
             CK(diomp_stream_sync(st[p]));
             bar.arrive_and_wait();
             CK(diomp_event_record(a, st[p]));
             for (int i = 0; i < iters; ++i) once(bytes);
+            exit_barrier();
             CK(diomp_event_record(b, st[p]));
             CK(diomp_event_sync(b));
             float m; CK(diomp_event_elapsed_ms(a, b, &m));

@@ -34,7 +34,7 @@ def main():
     for _ in range(n):
         coll.allreduce(comm, send.addr, recv.addr, 256, op, blocking=False)
     t1 = time.perf_counter()
-    s.synchronize()
+    coll.complete(comm)
     t2 = time.perf_counter()
     out["allreduce_enqueue_us"] = (t1 - t0) / n * 1e6
     out["allreduce_drain_us"] = (t2 - t0) / n * 1e6
@@ -71,7 +71,7 @@ def main():
     for _ in range(n):
         coll.allreduce(comm, send.addr, recv.addr, 256, op, blocking=False)
     pr.disable()
-    s.synchronize()
+    coll.complete(comm)
     if rt.rank == 0:
         print(out, flush=True)
         pstats.Stats(pr).sort_stats("tottime").print_stats(22)
