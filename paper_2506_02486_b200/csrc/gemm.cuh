@@ -20,6 +20,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "dgemm_tma.cuh"
 
 namespace diomp {
 namespace gemm {
@@ -384,6 +385,14 @@ int diomp_dgemm(const diomp_dgemm_args *x, void *stream) {
     // 16 warps of 32x32 in a 128x128 CTA (4 stages, 1 CTA/SM): 0.81-0.83.
     // B pitch BN+2 removed the paired-k B loads' 2-way bank conflicts (1.07e9 ->
     // 1.1e6 at 8192^3) for only +0.3 %: the gap to cuBLAS is not shared memory.
+    // default: the warp-specialised TMA kernel (dgemm_tma.cuh); the cp.async
+    // kernels below serve the fused-forward / device-flag ring step, operands
+    // TMA cannot describe, and DIOMP_DGEMM_TMA=0
+    static const bool tma_on = [] {
+        const char *e = getenv("DIOMP_DGEMM_TMA");
+        return !(e && atoi(e) == 0);
+    }();
+    if (tma_on && gemm_tma::eligible(x)) return gemm_tma::launch(x, (cudaStream_t)stream);
     if (!vec) return launch_dgemm<CfgP2, false>(p, x->device, (cudaStream_t)stream);
     const char *v = getenv("DIOMP_DGEMM_CFG");
     if (v && atoi(v) == 0) return launch_dgemm<CfgBig>(p, x->device, (cudaStream_t)stream);

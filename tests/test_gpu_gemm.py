@@ -38,7 +38,8 @@ def test_matmul_seam_vs_oracle_odd_shape():
 
 
 @pytest.mark.parametrize("mnk", [(128, 128, 16), (256, 384, 512), (200, 130, 66), (1024, 2048, 512),
-                                 (45, 90, 45), (129, 77, 33), (1, 1, 1), (3, 5, 0)])
+                                 (45, 90, 45), (129, 77, 33), (1, 1, 1), (3, 5, 0),
+                                 (130, 258, 34), (1000, 1002, 998), (7, 2, 2)])
 def test_dgemm_accumulate_rel_l2(mnk):
     import torch
 
