@@ -204,6 +204,28 @@ int diomp_reduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, u
 int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off,
                     uint64_t count, int32_t dtype, int32_t op, void *stream);
 
+/* Small messages: one-shot low-latency (LL) allreduce / bcast for teams of
+ * k <= 8 on distinct GPUs.  Every 4-byte payload word travels with its flag
+ * in one 8-byte store, (epoch << 32) | word, into the receiver's LL slot for
+ * the sender (two parities per slot), so a call needs no entry or exit
+ * handshake: allreduce = every position stores its vector to every peer,
+ * then folds all k in the reference order (bit-identical); bcast = the root
+ * stores to every non-root.  epoch_to[q] / epoch_from[q] = this call's epoch
+ * for the pair (both ends count every LL call between them, from 1); the
+ * LL region is `ll_off` in every member's segment, slot_bytes per (source
+ * endpoint, parity), at least 2x the payload.                               */
+typedef struct {
+    int32_t k, pos, device, dtype, op, root, mode;  /* mode 0 allreduce, 1 bcast (bytes) */
+    int32_t _pad;
+    uint64_t base[DIOMP_MAX_TEAM];
+    uint32_t slot[DIOMP_MAX_TEAM];
+    uint32_t epoch_to[DIOMP_MAX_TEAM];
+    uint32_t epoch_from[DIOMP_MAX_TEAM];
+    uint64_t ll_off, slot_bytes;
+    uint64_t send_off, recv_off, count;
+} diomp_ll_args;
+int diomp_ll_collective(const diomp_ll_args *args, void *stream);
+
 #ifdef DIOMP_EXPERIMENTS
 /* ---- Experiments build only (-DDIOMP_EXPERIMENTS; measured slower than the
  *      defaults on B200, kept out of the product library).

@@ -35,6 +35,15 @@ class NvlsArgs(ctypes.Structure):
                 ("epoch", c_u64), ("counter", c_u64)]
 
 
+class LLArgs(ctypes.Structure):
+    _fields_ = [("k", c_i32), ("pos", c_i32), ("device", c_i32), ("dtype", c_i32),
+                ("op", c_i32), ("root", c_i32), ("mode", c_i32), ("_pad", c_i32),
+                ("base", c_u64 * MAX_TEAM), ("slot", c_u32 * MAX_TEAM),
+                ("epoch_to", c_u32 * MAX_TEAM), ("epoch_from", c_u32 * MAX_TEAM),
+                ("ll_off", c_u64), ("slot_bytes", c_u64),
+                ("send_off", c_u64), ("recv_off", c_u64), ("count", c_u64)]
+
+
 class StencilArgs(ctypes.Structure):
     _fields_ = [("u_next", c_u64), ("u_cur", c_u64), ("u_prev", c_u64),
                 ("NX", c_i64), ("NY", c_i64), ("NZ", c_i64),
@@ -123,6 +132,7 @@ _PROTOS = {
     "diomp_bcast": [ctypes.POINTER(Team), c_u64, c_u64, c_i32, c_vp],
     "diomp_reduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_i32, c_vp],
     "diomp_allreduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_vp],
+    "diomp_ll_collective": [ctypes.POINTER(LLArgs), c_vp],
     "diomp_stencil_update": [ctypes.c_int, ctypes.POINTER(StencilArgs), c_vp],
     "diomp_stencil_run": [ctypes.POINTER(StencilPlan), c_i64, c_i64, c_vp],
     "diomp_matmul_f64": [ctypes.c_int, c_i64, c_i64, c_i64, c_u64, c_u64, c_u64, c_vp],

@@ -31,7 +31,7 @@ import numpy as np
 from . import _native
 from .errors import InvalidAddress, RootOutOfRange, StaleGroup, TypeMismatch, UsageError
 from .global_memory import GlobalAddress
-from .runtime import CHANNEL_COLL, COUNTER_COLL, COUNTER_OFF, Group, Runtime
+from .runtime import CHANNEL_COLL, CHANNEL_LL, COUNTER_COLL, COUNTER_OFF, LL_OFF, Group, Runtime
 from .topology import Endpoint
 
 
@@ -191,14 +191,78 @@ def _torch_stream(gpu: int) -> int:
     return raw(gpu) if raw is not None else torch.cuda.current_stream(gpu).cuda_stream
 
 
-def _advance(comm: Communicator, n: int):
+def _advance(comm: Communicator, n: int, channel: int = CHANNEL_COLL):
     rt = comm.rt
     for pos in comm.my_positions:
         me_ep = comm.ring[pos]
         me = rt.endpoint_index(me_ep.rank, me_ep.device)
         for q, ep in enumerate(comm.ring):
             if q != pos:
-                rt.advance_pair(me, rt.endpoint_index(ep.rank, ep.device), n, CHANNEL_COLL)
+                rt.advance_pair(me, rt.endpoint_index(ep.rank, ep.device), n, channel)
+
+
+# ---- one-shot low-latency (LL) path for small messages ---------------------
+LL_MAX_BYTES = int(os.environ.get("DIOMP_LL_MAX", str(32 * 1024)))
+
+
+def _ll_slot_bytes(comm: Communicator) -> int:
+    """Bytes per (source endpoint, parity) LL slot in the runtime scratch, or 0
+    when the LL path is unavailable for this communicator."""
+    v = comm.__dict__.get("_ll_slot")
+    if v is None:
+        rt = comm.rt
+        w = rt.nranks * rt.cfg.devices_per_rank
+        avail = rt._scratch_bytes - LL_OFF
+        v = (avail // (2 * w)) // 256 * 256 if avail > 0 else 0
+        # the experiments build's chain-bcast flags share this scratch
+        if not (comm.device_sync and 2 <= comm.size <= 8) or _native.has_experiments():
+            v = 0
+        comm._ll_slot = v
+    return v
+
+
+def _ll_ok(comm: Communicator, nbytes: int) -> bool:
+    slot = _ll_slot_bytes(comm)
+    return slot > 0 and nbytes <= LL_MAX_BYTES and (nbytes + 3) // 4 * 8 <= slot
+
+
+def _ll_run(comm: Communicator, mode: int, send_off: int, recv_off: int, count: int,
+            dtype: int, op: int, root: int, blocking: bool):
+    rt = comm.rt
+    if comm.__dict__.get("_pending"):
+        _exit(comm)   # a two-phase call still owes its exit: its stores may be in flight
+    slot = _ll_slot_bytes(comm)
+    cache = comm.__dict__.setdefault("_ll_args", {})
+    used = []
+    for pos in comm.my_positions:
+        me_ep = comm.ring[pos]
+        me = rt.endpoint_index(me_ep.rank, me_ep.device)
+        x = cache.get(pos)
+        if x is None:
+            x = _native.LLArgs()
+            x.k, x.pos, x.device = comm.size, pos, rt.gpus[me_ep.device]
+            for q, ep in enumerate(comm.ring):
+                x.base[q] = rt.peer_address(ep.rank, ep.device)
+                x.slot[q] = rt.endpoint_index(ep.rank, ep.device)
+            x.ll_off = rt.scratch_offset + LL_OFF
+            x.slot_bytes = slot
+            cache[pos] = x
+        for q in range(comm.size):
+            if q != pos:
+                sent, recvd = rt.pair_epochs(me, x.slot[q], CHANNEL_LL)
+                x.epoch_to[q] = (sent + 1) & 0xFFFFFFFF
+                x.epoch_from[q] = (recvd + 1) & 0xFFFFFFFF
+        x.mode, x.dtype, x.op, x.root = mode, dtype, op, root
+        x.send_off, x.recv_off, x.count = send_off, recv_off, count
+        s = rt._rma_streams[me_ep.device]
+        _after_torch(rt, me_ep.device)
+        _native.check(_native.lib.diomp_ll_collective(x, s.handle), "ll collective")
+        used.append(s)
+    _advance(comm, 1, CHANNEL_LL)
+    if blocking:
+        for s in used:
+            s.synchronize()
+            _native.check_device(s.gpu, "collective")
 
 
 def _exit(comm: Communicator):
@@ -290,6 +354,9 @@ def bcast(comm: Communicator, buffer: GlobalAddress, nbytes: int, root: int = 0,
     if k == 1 or nbytes == 0:
         return
     comm._next_seq()
+    if _ll_ok(comm, nbytes):
+        _ll_run(comm, 1, buffer.offset, buffer.offset, nbytes, 0, 0, root, blocking)
+        return
     _run(comm, lambda t, s: _native.lib.diomp_bcast(t, buffer.offset, nbytes, root, s), blocking)
 
 
@@ -339,8 +406,7 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
     if memo.get(key) == rt._ledger_gen and k > 1 and algo == "exact":
         # same call shape validated since the last allocation change
         comm._next_seq()
-        _run(comm, lambda t, s: _native.lib.diomp_allreduce(
-            t, send.offset, recv.offset, count, op.etype.code, op.code, s), blocking)
+        _allreduce_exact(comm, send, recv, count, op, blocking)
         return
     _check_typed(send, count, op.etype)
     _check_typed(recv, count, op.etype)
@@ -371,6 +437,14 @@ def allreduce(comm: Communicator, send: GlobalAddress, recv: GlobalAddress, coun
         _allreduce_nvls(comm, send, recv, count, op, blocking)
         return
     memo[key] = rt._ledger_gen
+    _allreduce_exact(comm, send, recv, count, op, blocking)
+
+
+def _allreduce_exact(comm, send, recv, count, op, blocking):
+    nbytes = count * op.etype.dtype.itemsize
+    if _ll_ok(comm, nbytes):
+        _ll_run(comm, 0, send.offset, recv.offset, count, op.etype.code, op.code, 0, blocking)
+        return
     _run(comm, lambda t, s: _native.lib.diomp_allreduce(t, send.offset, recv.offset, count,
                                                         op.etype.code, op.code, s), blocking)
 

@@ -578,6 +578,158 @@ static bool team_ok(const diomp_team *t) {
     return t->k >= 1 && t->k <= DIOMP_MAX_TEAM && t->pos >= 0 && t->pos < t->k;
 }
 
+// ---------------------------------------------------------------------------
+// Small messages: one-shot "LL" (low-latency) collectives.
+//
+// For a few KiB the two-phase kernel above is all handshake: entry round trip,
+// peer loads, stores.  Here every 4-byte payload word travels with its flag in
+// one 8-byte store, (epoch << 32) | word, so a receiver knows the word has
+// landed when its flag reads this call's epoch -- no separate signal, no
+// fence, no entry or exit handshake; one NVLink one-way trip per call.
+//   allreduce: every position stores its whole vector into every peer's LL
+//     slot, then folds all k vectors element by element in the reference's
+//     order (block b = [b*count/k, (b+1)*count/k) folded from position b), so
+//     each position computes the full result itself -- bit-identical.
+//   bcast: the root stores into every non-root's slot; non-roots copy out.
+// Slots: per source endpoint, two parities (epoch & 1).  Writing call n+2's
+// parity into a peer's slot is safe without a handshake: this position's call
+// n+1 received the peer's call n+1 words, so the peer's stream had finished
+// call n -- the last reader of that parity.  Epochs are per pair (both ends
+// count every LL call between them), flags start at 0 (segments are
+// zero-filled), epochs at 1.
+// ---------------------------------------------------------------------------
+
+struct LLArgs {
+    int32_t k, pos, dtype, op, root, mode;   // mode 0 allreduce, 1 bcast
+    uint64_t base[DIOMP_MAX_TEAM];           // position's segment base (as addressable here)
+    uint32_t slot[DIOMP_MAX_TEAM];           // position's global endpoint index
+    uint32_t ep_to[DIOMP_MAX_TEAM];          // this call's epoch toward position q
+    uint32_t ep_from[DIOMP_MAX_TEAM];        // this call's epoch from position q
+    uint64_t ll_off, slot_bytes;             // LL region offset; bytes per (slot, parity)
+    uint64_t send_off, recv_off, count;      // elements (bytes for bcast)
+};
+
+__device__ __forceinline__ uint64_t *ll_slot(const LLArgs &a, int at, int from, uint32_t epoch) {
+    return (uint64_t *)(a.base[at] + a.ll_off + ((uint64_t)a.slot[from] * 2 + (epoch & 1)) * a.slot_bytes);
+}
+
+__device__ __forceinline__ uint32_t ll_wait(const uint64_t *p, uint32_t epoch) {
+    uint64_t v;
+    const uint64_t t0 = globaltimer_ns();
+    for (;;) {
+        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+        if ((uint32_t)(v >> 32) == epoch) return (uint32_t)v;
+        if (globaltimer_ns() - t0 > g_wait_timeout_ns) {
+            record_device_error((unsigned)DIOMP_INTERNAL);
+            return 0;
+        }
+    }
+}
+
+__device__ __forceinline__ void ll_store(uint64_t *p, uint32_t epoch, uint32_t w) {
+    const uint64_t v = ((uint64_t)epoch << 32) | w;
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <typename T, typename OP, int KMAX>
+__global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant__ LLArgs a) {
+    constexpr int W = sizeof(T) / 4;
+    const int k = a.k, me = a.pos;
+    const uint64_t n = a.count;
+    const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gsz = (uint64_t)gridDim.x * blockDim.x;
+    const T *send = (const T *)(a.base[me] + a.send_off);
+    T *recv = (T *)(a.base[me] + a.recv_off);
+    // push my vector into every peer's slot
+    for (uint64_t e = gtid; e < n; e += gsz) {
+        uint32_t w[W];
+        const T v = send[e];
+        memcpy(w, &v, sizeof(T));
+        for (int q = 0; q < k; ++q) {
+            if (q == me) continue;
+            uint64_t *dst = ll_slot(a, q, me, a.ep_to[q]) + e * W;
+#pragma unroll
+            for (int i = 0; i < W; ++i) ll_store(dst + i, a.ep_to[q], w[i]);
+        }
+    }
+    // gather every position's element and fold in the reference order
+    for (uint64_t e = gtid; e < n; e += gsz) {
+        T vals[KMAX];
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q) {
+            if (q >= k) break;
+            if (q == me) {
+                vals[q] = send[e];
+            } else {
+                const uint64_t *src = ll_slot(a, me, q, a.ep_from[q]) + e * W;
+                uint32_t w[W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) w[i] = ll_wait(src + i, a.ep_from[q]);
+                memcpy(&vals[q], w, sizeof(T));
+            }
+        }
+        int b = (int)(e * (uint64_t)k / n);
+        while (b + 1 < k && (uint64_t)(b + 1) * n / k <= e) ++b;
+        while (b > 0 && (uint64_t)b * n / k > e) --b;
+        T acc = vals[b];
+        for (int i = 1; i < k; ++i) {
+            int q = b + i;
+            if (q >= k) q -= k;
+#pragma unroll
+            for (int qq = 0; qq < KMAX; ++qq)   // register-resident select of vals[q]
+                if (qq == q) acc = OP::apply(acc, vals[qq]);
+        }
+        recv[e] = acc;
+    }
+}
+
+// bcast of `count` bytes at send_off: the root stores 4-byte words (zero-padded
+// tail) into every non-root's slot; non-roots copy them into their buffer.
+__global__ void __launch_bounds__(256) ll_bcast_kernel(const __grid_constant__ LLArgs a) {
+    const int k = a.k, me = a.pos, root = a.root;
+    const uint64_t nw = (a.count + 3) / 4;
+    const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gsz = (uint64_t)gridDim.x * blockDim.x;
+    uint8_t *buf = (uint8_t *)(a.base[me] + a.send_off);
+    if (me == root) {
+        for (uint64_t i = gtid; i < nw; i += gsz) {
+            uint32_t w = 0;
+            const uint64_t o = i * 4;
+            for (int b = 0; b < 4 && o + b < a.count; ++b) w |= (uint32_t)buf[o + b] << (8 * b);
+            for (int q = 0; q < k; ++q)
+                if (q != root) ll_store(ll_slot(a, q, root, a.ep_to[q]) + i, a.ep_to[q], w);
+        }
+        return;
+    }
+    const uint64_t *src = ll_slot(a, me, root, a.ep_from[root]);
+    for (uint64_t i = gtid; i < nw; i += gsz) {
+        const uint32_t w = ll_wait(src + i, a.ep_from[root]);
+        const uint64_t o = i * 4;
+        for (int b = 0; b < 4 && o + b < a.count; ++b) buf[o + b] = (uint8_t)(w >> (8 * b));
+    }
+}
+
+template <typename T, typename OP>
+static int launch_ll(const LLArgs &a, cudaStream_t s) {
+    const int64_t blocks = std::min<int64_t>(ceil_div((int64_t)a.count, 256), 32);
+    if (a.k <= 2) ll_allreduce_kernel<T, OP, 2><<<(unsigned)blocks, 256, 0, s>>>(a);
+    else if (a.k <= 4) ll_allreduce_kernel<T, OP, 4><<<(unsigned)blocks, 256, 0, s>>>(a);
+    else if (a.k <= 8) ll_allreduce_kernel<T, OP, 8><<<(unsigned)blocks, 256, 0, s>>>(a);
+    else return DIOMP_BAD_REQUEST;
+    DIOMP_LAUNCH_CHECK();
+    return DIOMP_OK;
+}
+
+template <typename T>
+static int ll_dispatch_op(const LLArgs &a, cudaStream_t s) {
+    switch (a.op) {
+        case DIOMP_SUM: return launch_ll<T, Sum<T>>(a, s);
+        case DIOMP_MIN: return launch_ll<T, Min<T>>(a, s);
+        case DIOMP_MAX: return launch_ll<T, Max<T>>(a, s);
+        default: return DIOMP_BAD_REQUEST;
+    }
+}
+
 }  // namespace coll
 }  // namespace diomp
 
@@ -631,6 +783,45 @@ int diomp_reduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off, u
     a.root = root;
     a.mode = 1;
     return dispatch(a, dtype, op, (cudaStream_t)stream);
+}
+
+int diomp_ll_collective(const diomp_ll_args *x, void *stream) {
+    using namespace diomp;
+    using namespace diomp::coll;
+    if (x->k < 1 || x->k > 8 || x->pos < 0 || x->pos >= x->k || x->root < 0 || x->root >= x->k)
+        return DIOMP_BAD_REQUEST;
+    if (x->count == 0 || x->k == 1) return DIOMP_OK;
+    LLArgs a{};
+    a.k = x->k; a.pos = x->pos; a.dtype = x->dtype; a.op = x->op; a.root = x->root;
+    a.mode = x->mode;
+    for (int q = 0; q < x->k; ++q) {
+        a.base[q] = x->base[q];
+        a.slot[q] = x->slot[q];
+        a.ep_to[q] = x->epoch_to[q];
+        a.ep_from[q] = x->epoch_from[q];
+    }
+    a.ll_off = x->ll_off;
+    a.slot_bytes = x->slot_bytes;
+    a.send_off = x->send_off;
+    a.recv_off = x->recv_off;
+    a.count = x->count;
+    const uint64_t esz = x->mode == 1 ? 1 : (x->dtype == DIOMP_F64 || x->dtype == DIOMP_I64 ? 8 : 4);
+    if ((x->count * esz + 3) / 4 * 8 > x->slot_bytes) return DIOMP_BAD_REQUEST;   // LL doubles the bytes
+    DIOMP_CUDA_TRY(cudaSetDevice(x->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (x->mode == 1) {
+        const int64_t blocks = std::min<int64_t>(ceil_div((int64_t)(x->count + 3) / 4, 256), 32);
+        ll_bcast_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+        DIOMP_LAUNCH_CHECK();
+        return DIOMP_OK;
+    }
+    switch (x->dtype) {
+        case DIOMP_F32: return ll_dispatch_op<float>(a, s);
+        case DIOMP_F64: return ll_dispatch_op<double>(a, s);
+        case DIOMP_I32: return ll_dispatch_op<int32_t>(a, s);
+        case DIOMP_I64: return ll_dispatch_op<int64_t>(a, s);
+        default: return DIOMP_BAD_REQUEST;
+    }
 }
 
 int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_t root, void *stream) {

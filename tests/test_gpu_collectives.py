@@ -353,3 +353,69 @@ def test_absent_peer_surfaces_transport_failure_at_the_deadline():
     res = run_emulated(2, fn, segment_bytes=64 * MIB, timeout=30.0)
     assert res[0][0] == "TransportFailure", res[0]
     assert 0.4 < res[0][1] < 10.0, res[0]
+
+
+@need_gpus(2)
+def test_small_message_ll_path_bitwise_back_to_back():
+    """One-shot LL collectives (payload + flag in one 8-byte store, no
+    handshakes) for small messages: bitwise equal to the reference fold for
+    every dtype/op, in place and out of place, 300 back-to-back non-blocking
+    calls interleaved with two-phase (large) allreduces and LL / two-phase
+    bcasts -- the LL slot parities and the two-phase exit bookkeeping must
+    never let a call see another call's bytes."""
+    from oracle import oracle as O
+    from paper_2506_02486_b200 import GlobalAddress
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200.emulate import run_emulated
+    k = min(NGPU, 4)
+    plan = []
+    for i in range(300):
+        et = ("f32", "f64", "i32", "i64")[i % 4]
+        kind = ("sum", "min", "max")[i % 3]
+        count = (1, 3, 257, 1000, 4093, 300_001)[i % 6]
+        plan.append((et, kind, count, i % 5 == 0))
+
+    def contrib(r, et, count, i):
+        rng = np.random.default_rng(4000 + 7 * i + r)
+        if et[0] == "f":
+            return rng.uniform(-1, 1, count).astype(DT[et])
+        return rng.integers(-2**30, 2**30, count).astype(DT[et])
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        assert comm.device_sync
+        bufs = [rt.alloc_symmetric(3 * MIB, 0) for _ in range(6)]
+        bc = rt.alloc_symmetric(64 * 1024, 0)
+        outs = []
+        for i, (et, kind, count, in_place) in enumerate(plan):
+            op = coll.ReduceOp(coll.ReduceKind(kind), coll.ElementType(et))
+            isz = np.dtype(DT[et]).itemsize
+            send = bufs[(2 * i) % 6]
+            recv = send if in_place else bufs[(2 * i + 1) % 6]
+            v = contrib(rt.rank, et, count, i)
+            rt.gm.view(0, send.addr.offset, v.nbytes)[:] = v.tobytes()
+            coll.allreduce(comm, send.addr, recv.addr, count, op, blocking=False)
+            if i % 7 == 3:   # an LL-sized bcast from a rotating root
+                nb = 1 + (i * 37) % 5000
+                root = i % comm.size
+                mine = np.random.default_rng(9000 + i + rt.rank).integers(
+                    0, 256, nb, dtype=np.uint8)
+                coll.complete(comm)
+                rt.gm.view(0, bc.addr.offset, nb)[:] = mine.tobytes()
+                coll.bcast(comm, bc.addr, nb, root=root)
+                outs.append(("bc", i, mine.tobytes() if rt.rank == root else None,
+                             bytes(rt.gm.view(0, bc.addr.offset, nb))))
+            coll.complete(comm)
+            outs.append(("ar", i, bytes(rt.gm.view(0, recv.addr.offset, count * isz))))
+        return outs
+
+    res = run_emulated(k, fn, segment_bytes=64 * MIB)
+    for j, item in enumerate(res[0]):
+        if item[0] == "ar":
+            _, i, _ = item
+            et, kind, count, _ = plan[i]
+            want = O.allreduce_fold([contrib(r, et, count, i) for r in range(k)], kind).tobytes()
+            assert all(r[j][2] == want for r in res), (i, et, kind, count)
+        else:
+            snap = next(r[j][2] for r in res if r[j][2] is not None)
+            assert all(r[j][3] == snap for r in res), item[1]

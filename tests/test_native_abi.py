@@ -45,7 +45,7 @@ def test_struct_layouts_match_header():
     from paper_2506_02486_b200 import _native
     src = ('#include <stdio.h>\n#include "diomp_b200.h"\nint main(){printf("%zu %zu %zu %zu\\n",'
            'sizeof(diomp_team),sizeof(diomp_stencil_args),sizeof(diomp_stencil_plan),'
-           'sizeof(diomp_dgemm_args));return 0;}\n')
+           'sizeof(diomp_dgemm_args));printf("%zu\\n",sizeof(diomp_ll_args));return 0;}\n')
     tmp = os.path.join(ROOT, "build")
     os.makedirs(tmp, exist_ok=True)
     c, exe = os.path.join(tmp, "sz.c"), os.path.join(tmp, "sz")
@@ -53,7 +53,7 @@ def test_struct_layouts_match_header():
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
     got = [int(x) for x in subprocess.check_output([exe]).split()]
     want = [ctypes.sizeof(t) for t in (_native.Team, _native.StencilArgs, _native.StencilPlan,
-                                        _native.DgemmArgs)]
+                                        _native.DgemmArgs, _native.LLArgs)]
     assert got == want
 
 
