@@ -7,22 +7,25 @@
 // reference's order (acc = c*u; x taps t=1..4; y taps; z taps;
 // (2u - u_prev) + acc), so no FMA contraction can occur.
 //
-// Fast path (R=4, NZ even, 16 B aligned): one CTA per SM owns a 24(y) x 64(z)
+// Fast path (R=4, NZ even, 16 B aligned): one CTA per SM owns a 14(y) x 128(z)
 // column of the domain and streams along x through a chunk of planes.  The CTA
 // is warp-specialised:
 //   * a producer warp issues TMA (cp.async.bulk.tensor.3d) loads: u_cur plane
-//     tiles with their 4-wide y/z halo (32 x 72 f64) into an 8-slot ring and
-//     u_prev tiles (24 x 64) into a 5-slot ring, each slot with a "full"
-//     (transaction-count) and an "empty" (consumer-arrival) mbarrier -- no
-//     CTA-wide barrier per plane;
-//   * 12 compute warps, 2(y) x 2(z) points per thread, keep the 9-plane
-//     x-window of each point in registers (the plane loop is unrolled 9x so the
-//     window rotates by register renaming; 128 registers, no spills); y/z taps
-//     come from the centre plane's slot with 16 B shared loads (conflict-free
-//     rows), interleaved tap by tap so only a sliding pair of rows is live;
+//     tiles with their 4-wide y/z halo (22 x 136 f64, 1088-byte rows) into a
+//     7-slot ring and u_prev tiles (14 x 128) into a 4-slot ring, each slot
+//     with a "full" (transaction-count) and an "empty" (consumer-arrival)
+//     mbarrier -- no CTA-wide barrier per plane;
+//   * 14 compute warps (7 row pairs x 2 halves of the 128 columns), 2(y) x 2(z)
+//     points per thread, keep the 9-plane x-window of each point in registers
+//     (the plane loop is unrolled 9x so the window rotates by register
+//     renaming; 128 registers, no spills); y/z taps come from the centre
+//     plane's slot with 16 B shared loads (conflict-free rows), interleaved
+//     tap by tap so only a sliding pair of rows is live;
 //   * u_next is stored with 16 B coalesced stores.
-// Measured (1024^3, one B200): 246 Gpts/s, DRAM traffic 1.04x the 24 B/point
-// algorithmic minimum (profiles/r01_stencil_v6_full_summary.json).
+// Measured (1024^3, one B200): 258.6 Gpts/s = 0.947 of the measured HBM copy
+// peak at 24 B/point.  Round 1's 24 x 64 tiles (576-byte TMA rows, 12 compute
+// warps) ran 243-246: the longer rows and the two extra compute warps are
+// each worth about half of the gain (profiles/r02_stencil_shapes.txt).
 // Fused driver epilogue: output planes [R,2R) / [nxl, nxl+R) are also stored
 // into the left / right neighbour's u_next ghost planes over NVLink (peer
 // pointers), the point source is added in-register (one extra rounded add,
@@ -47,15 +50,19 @@ namespace stencil {
 
 constexpr int R = 4;
 #ifndef DIOMP_STENCIL_NCW
-#define DIOMP_STENCIL_NCW 12
+#define DIOMP_STENCIL_NCW 14
 #endif
-constexpr int NCW = DIOMP_STENCIL_NCW;  // compute warps (2 rows each)
-constexpr int TY = 2 * NCW;
-constexpr int TZ = 64;
+constexpr int NCW = DIOMP_STENCIL_NCW;  // compute warps (2 rows x 64 columns each)
+#ifndef DIOMP_STENCIL_WZ
+#define DIOMP_STENCIL_WZ 2
+#endif
+constexpr int WZ = DIOMP_STENCIL_WZ;    // compute warps side by side along z
+constexpr int TY = 2 * NCW / WZ;
+constexpr int TZ = 64 * WZ;
 constexpr int BY = TY + 2 * R;  // rows per slot
-constexpr int BZ = TZ + 2 * R;  // 72 columns per slot
+constexpr int BZ = TZ + 2 * R;  // columns per slot
 constexpr int SLOT = BY * BZ;   // doubles per slot
-// smem budget (227 KB): u_cur ring of BY x 72 tiles + u_prev ring of TY x 64 tiles
+// smem budget (227 KB): u_cur ring of BY x BZ tiles + u_prev ring of TY x TZ tiles
 #ifndef DIOMP_STENCIL_NSLOT
 #define DIOMP_STENCIL_NSLOT (NCW >= 16 ? 7 : (NCW >= 14 ? 7 : (NCW >= 12 ? 8 : 11)))
 #endif
@@ -71,6 +78,9 @@ constexpr uint32_t SLOT_BYTES = SLOT * 8;
 constexpr uint32_t PSLOT_BYTES = PSLOT * 8;
 constexpr size_t SMEM_BYTES =
     (size_t)NSLOT * SLOT_BYTES + (size_t)NPREV * PSLOT_BYTES + 2 * (NSLOT + NPREV) * 8;
+static_assert(SMEM_BYTES <= 232448, "stencil rings exceed 227 KB of shared memory");
+static_assert(BZ <= 256 && BY <= 256, "TMA box dimensions are at most 256");
+static_assert(NCW % WZ == 0, "compute warps must tile the rows evenly");
 
 struct Params {
     double *u_next;
@@ -373,7 +383,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else {
         // ---- compute warps: 2 rows x 64 columns each, 2x2 points per thread
-        const int ry = 2 * warp, zz = 2 * lane;
+        const int ry = 2 * (warp / WZ), zz = 64 * (warp % WZ) + 2 * lane;
         const int64_t y = y0 + ry, z = z0 + zz;
         Lane ln;
         ln.yv0 = y < p.NY - R;
