@@ -225,6 +225,15 @@ typedef struct {
     uint64_t send_off, recv_off, count;
 } diomp_ll_args;
 int diomp_ll_collective(const diomp_ll_args *args, void *stream);
+/* The same call as the runtime issues it, in one C call (replaces the
+ * per-call Python of collectives.py:326-405's small-message path): epochs
+ * taken from -- and advanced in -- the RMA context's per-pair LL table
+ * (args->epoch_* are outputs), `stream` ordered after `after` (the caller's
+ * stream, by an event; NULL = no ordering), and with blocking != 0 the
+ * stream drained and the device error word checked (DIOMP_INTERNAL = a
+ * device-side wait timed out: TransportFailure).                          */
+int diomp_ll_call(void *rma_ctx, diomp_ll_args *args, void *stream, void *after,
+                  int32_t blocking);
 
 #ifdef DIOMP_EXPERIMENTS
 /* ---- Experiments build only (-DDIOMP_EXPERIMENTS; measured slower than the

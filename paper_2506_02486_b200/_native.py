@@ -133,6 +133,7 @@ _PROTOS = {
     "diomp_reduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_i32, c_vp],
     "diomp_allreduce": [ctypes.POINTER(Team), c_u64, c_u64, c_u64, c_i32, c_i32, c_vp],
     "diomp_ll_collective": [ctypes.POINTER(LLArgs), c_vp],
+    "diomp_ll_call": [c_vp, ctypes.POINTER(LLArgs), c_vp, c_vp, c_i32],
     "diomp_stencil_update": [ctypes.c_int, ctypes.POINTER(StencilArgs), c_vp],
     "diomp_stencil_run": [ctypes.POINTER(StencilPlan), c_i64, c_i64, c_vp],
     "diomp_matmul_f64": [ctypes.c_int, c_i64, c_i64, c_i64, c_u64, c_u64, c_u64, c_vp],

@@ -22,6 +22,7 @@ each other must never share a GPU.
 
 from __future__ import annotations
 
+import ctypes
 import enum
 import os
 from dataclasses import dataclass
@@ -31,7 +32,7 @@ import numpy as np
 from . import _native
 from .errors import InvalidAddress, RootOutOfRange, StaleGroup, TypeMismatch, UsageError
 from .global_memory import GlobalAddress
-from .runtime import CHANNEL_COLL, CHANNEL_LL, COUNTER_COLL, COUNTER_OFF, LL_OFF, Group, Runtime
+from .runtime import CHANNEL_COLL, COUNTER_COLL, COUNTER_OFF, LL_OFF, Group, Runtime
 from .topology import Endpoint
 
 
@@ -226,19 +227,16 @@ def _ll_ok(comm: Communicator, nbytes: int) -> bool:
     return slot > 0 and nbytes <= LL_MAX_BYTES and (nbytes + 3) // 4 * 8 <= slot
 
 
-def _ll_run(comm: Communicator, mode: int, send_off: int, recv_off: int, count: int,
-            dtype: int, op: int, root: int, blocking: bool):
-    rt = comm.rt
-    if comm.__dict__.get("_pending"):
-        _exit(comm)   # a two-phase call still owes its exit: its stores may be in flight
-    slot = _ll_slot_bytes(comm)
-    cache = comm.__dict__.setdefault("_ll_args", {})
-    used = []
-    for pos in comm.my_positions:
-        me_ep = comm.ring[pos]
-        me = rt.endpoint_index(me_ep.rank, me_ep.device)
-        x = cache.get(pos)
-        if x is None:
+def _ll_calls(comm: Communicator) -> list:
+    """Per local position: (LLArgs, RMA stream, GPU) -- built once per
+    communicator; the per-call work is one C call per position."""
+    calls = comm.__dict__.get("_ll_calls")
+    if calls is None:
+        rt = comm.rt
+        slot = _ll_slot_bytes(comm)
+        calls = []
+        for pos in comm.my_positions:
+            me_ep = comm.ring[pos]
             x = _native.LLArgs()
             x.k, x.pos, x.device = comm.size, pos, rt.gpus[me_ep.device]
             for q, ep in enumerate(comm.ring):
@@ -246,23 +244,35 @@ def _ll_run(comm: Communicator, mode: int, send_off: int, recv_off: int, count: 
                 x.slot[q] = rt.endpoint_index(ep.rank, ep.device)
             x.ll_off = rt.scratch_offset + LL_OFF
             x.slot_bytes = slot
-            cache[pos] = x
-        for q in range(comm.size):
-            if q != pos:
-                sent, recvd = rt.pair_epochs(me, x.slot[q], CHANNEL_LL)
-                x.epoch_to[q] = (sent + 1) & 0xFFFFFFFF
-                x.epoch_from[q] = (recvd + 1) & 0xFFFFFFFF
+            calls.append((x, ctypes.byref(x), rt._rma_streams[me_ep.device], rt.gpus[me_ep.device]))
+        comm._ll_calls = calls
+    return calls
+
+
+def _ll_run(comm: Communicator, mode: int, send_off: int, recv_off: int, count: int,
+            dtype: int, op: int, root: int, blocking: bool):
+    """One LL call: diomp_ll_call per local position does the epochs (kept in
+    the native RMA context, per endpoint pair), the ordering after torch's
+    stream, the launch and -- for a blocking call on one position -- the wait
+    and the device error check."""
+    rt = comm.rt
+    if comm.__dict__.get("_pending"):
+        _exit(comm)   # a two-phase call still owes its exit: its stores may be in flight
+    calls = _ll_calls(comm)
+    one = len(calls) == 1
+    ll_call = _native.lib.diomp_ll_call
+    for x, xref, s, gpu in calls:
         x.mode, x.dtype, x.op, x.root = mode, dtype, op, root
         x.send_off, x.recv_off, x.count = send_off, recv_off, count
-        s = rt._rma_streams[me_ep.device]
-        _after_torch(rt, me_ep.device)
-        _native.check(_native.lib.diomp_ll_collective(x, s.handle), "ll collective")
-        used.append(s)
-    _advance(comm, 1, CHANNEL_LL)
-    if blocking:
-        for s in used:
+        rc = ll_call(rt._rma_ctx, xref, s.handle, _torch_stream(gpu), 1 if (blocking and one) else 0)
+        if rc:   # DIOMP_INTERNAL: a device-side wait timed out -> TransportFailure
+            _native.check(rc, "collective")
+    if blocking and not one:
+        # every position's kernel is in flight before any wait (they wait on
+        # each other's words)
+        for _, _, s, gpu in calls:
             s.synchronize()
-            _native.check_device(s.gpu, "collective")
+            _native.check_device(gpu, "collective")
 
 
 def _exit(comm: Communicator):

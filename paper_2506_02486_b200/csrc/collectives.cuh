@@ -824,6 +824,60 @@ int diomp_ll_collective(const diomp_ll_args *x, void *stream) {
     }
 }
 
+// One LL call as the runtime issues it, in a single C call: this call's
+// epochs from the context's pair table (then advanced), the stream ordered
+// after the caller's `after` stream (an event, no host synchronisation), the
+// launch, and with `blocking` the wait for completion plus the device
+// error-word check (a timed-out device wait -> DIOMP_INTERNAL, the
+// reference's TransportFailure).  The Python equivalent cost ~11 us of
+// interpreter time per call (profiles/r02_coll_host_overhead_ll.txt).
+int diomp_ll_call(void *ctx, diomp_ll_args *x, void *stream, void *after, int32_t blocking) {
+    using namespace diomp;
+    auto *c = (rma::Ctx *)ctx;
+    if (!c || x->k < 1 || x->k > 8 || x->pos < 0 || x->pos >= x->k) return DIOMP_BAD_REQUEST;
+    const uint32_t n = (uint32_t)c->nranks * (uint32_t)c->dpr;
+    const uint32_t me = x->slot[x->pos];
+    for (int q = 0; q < x->k; ++q)
+        if (x->slot[q] >= n) return DIOMP_BAD_REQUEST;
+    if (x->count == 0 || x->k == 1) return DIOMP_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    DIOMP_CUDA_TRY(cudaSetDevice(x->device));
+    if (after && after != stream) {
+        cudaEvent_t ev;
+        {
+            std::lock_guard<std::mutex> lk(c->mu);
+            if ((int)c->order_ev.size() <= x->device) c->order_ev.resize(x->device + 1, nullptr);
+            if (!c->order_ev[x->device])
+                DIOMP_CUDA_TRY(cudaEventCreateWithFlags(&c->order_ev[x->device], cudaEventDisableTiming));
+            ev = c->order_ev[x->device];
+        }
+        // record + wait back to back on this thread: a later record on the
+        // same event cannot slip in between for this caller's ordering
+        DIOMP_CUDA_TRY(cudaEventRecord(ev, (cudaStream_t)after));
+        DIOMP_CUDA_TRY(cudaStreamWaitEvent(s, ev, 0));
+    }
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        for (int q = 0; q < x->k; ++q) {
+            if (q == x->pos) continue;
+            const uint32_t p = x->slot[q];
+            x->epoch_to[q] = c->ll_sent[me * n + p] + 1;
+            x->epoch_from[q] = c->ll_recvd[p * n + me] + 1;
+        }
+        int rc = diomp_ll_collective(x, stream);
+        if (rc) return rc;
+        for (int q = 0; q < x->k; ++q) {
+            if (q == x->pos) continue;
+            const uint32_t p = x->slot[q];
+            c->ll_sent[me * n + p] += 1;
+            c->ll_recvd[p * n + me] += 1;
+        }
+    }
+    if (!blocking) return DIOMP_OK;
+    DIOMP_CUDA_TRY(cudaStreamSynchronize(s));
+    return diomp_device_error(x->device);
+}
+
 int diomp_bcast(const diomp_team *team, uint64_t offset, uint64_t nbytes, int32_t root, void *stream) {
     using namespace diomp;
     using namespace diomp::coll;

@@ -55,6 +55,11 @@ struct Ctx {
     std::vector<uint32_t> free_slots;
     std::vector<uint32_t> live;            // slots with a pending op, issue order
     std::vector<std::vector<cudaEvent_t>> ev_pool;   // per CUDA device
+    // LL collective epochs per ordered endpoint pair: ll_sent[me * n + peer] =
+    // LL calls this endpoint made toward peer, ll_recvd[peer * n + me] = LL
+    // calls it took from peer (both ends count every call between them)
+    std::vector<uint32_t> ll_sent, ll_recvd;
+    std::vector<cudaEvent_t> order_ev;     // per CUDA device: "after the caller's stream"
     std::mutex mu;
 };
 
@@ -143,6 +148,9 @@ int diomp_rma_ctx_create(int32_t nranks, int32_t devices_per_rank, void **ctx_ou
     c->dpr = devices_per_rank;
     c->peers.resize((size_t)nranks * devices_per_rank);
     c->locals.resize(devices_per_rank);
+    const size_t n = (size_t)nranks * devices_per_rank;
+    c->ll_sent.assign(n * n, 0);
+    c->ll_recvd.assign(n * n, 0);
     *ctx_out = c;
     return DIOMP_OK;
 }
@@ -160,6 +168,8 @@ int diomp_rma_ctx_destroy(void *ctx) {
         c->live.clear();
         for (auto &pool : c->ev_pool)
             for (cudaEvent_t e : pool) cudaEventDestroy(e);
+        for (cudaEvent_t e : c->order_ev)
+            if (e) cudaEventDestroy(e);
     }
     delete c;
     return DIOMP_OK;
