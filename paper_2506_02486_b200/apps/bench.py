@@ -83,6 +83,27 @@ class BenchRow:
         return base + (f",{self.ratio:.4f}" if self.ratio is not None else "")
 
 
+def _pinned(src: np.ndarray | None = None, nbytes: int = 0) -> np.ndarray:
+    """A page-locked host buffer (a numpy view of pinned torch memory), filled
+    from `src` when given: host legs of the timed regions run from pinned
+    memory, as a production caller's would (pageable copies are staged by
+    the driver at a fraction of PCIe speed)."""
+    import torch
+    n = src.nbytes if src is not None else nbytes
+    buf = torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True).numpy()[:n]
+    if src is not None:
+        buf[:] = src.view(np.uint8).reshape(-1)
+        return buf.view(src.dtype)
+    return buf
+
+
+def bw_iters(size: int, base: int) -> int:
+    """Repetitions of one bandwidth row: at least `base`, and enough that the
+    timed region holds >= 2 GiB up to 32 reps (so a 64 MiB row is not
+    dominated by the first launch and the closing fence / handshake)."""
+    return max(base, min(32, (2 << 30) // max(size, 1)))
+
+
 class _Timer:
     """CUDA-event timer on the rank's RMA stream of device 0."""
 
@@ -123,6 +144,8 @@ def run_p2p(rt: Runtime, spec: BenchSpec) -> list[BenchRow]:
         for size in spec.sizes:
             payload = np.random.default_rng(size).integers(0, 256, size, dtype=np.uint8)
             sink = bytearray(size)
+            if not d2d:
+                payload, sink = _pinned(payload), _pinned(nbytes=size)
             if d2d:
                 rt.gm.view(0, src.addr.offset, size)[:] = payload.tobytes()
             for _ in range(spec.warmup):
@@ -399,8 +422,9 @@ def _coll_e2e(rt, kind: str, nbytes: int, reps: int = 3) -> dict:
     comm = coll.bootstrap(rt, rt.world)
     send = rt.alloc_symmetric(nbytes, 0)
     recv = rt.alloc_symmetric(nbytes, 0)
-    host = np.random.default_rng(2000 + rt.rank).uniform(-1, 1, nbytes // 4).astype(np.float32)
-    out = np.empty_like(host)
+    host = _pinned(np.random.default_rng(2000 + rt.rank).uniform(-1, 1, nbytes // 4)
+                   .astype(np.float32))
+    out = _pinned(nbytes=nbytes).view(np.float32)
     op = coll.ReduceOp(coll.ReduceKind.Sum, coll.ElementType.f32)
     me = GlobalAddress(rt.rank, 0, send.addr.offset)
     res = GlobalAddress(rt.rank, 0, (recv if kind == "allreduce" else send).addr.offset)
@@ -661,9 +685,12 @@ def measure_p2p(rt: Runtime, sizes=(8, 64 * MIB, 1 << 30), iters: int = 5) -> di
     big = [x for x in sizes if x >= MIB]
     res = {}
     for kind in (BenchKind.Bandwidth, BenchKind.GetBandwidth):
-        rows = run_p2p(rt, BenchSpec(kind, tuple(big), iters=iters, warmup=2,
-                                     transfer=TransferKind.D2D))
-        res[kind.value] = {r.size_bytes: round(r.size_bytes / r.mean_us / 1e3, 2) for r in rows}
+        res[kind.value] = {}
+        for size in big:
+            rows = run_p2p(rt, BenchSpec(kind, (size,), iters=bw_iters(size, iters), warmup=2,
+                                         transfer=TransferKind.D2D))
+            res[kind.value].update({r.size_bytes: round(r.size_bytes / r.mean_us / 1e3, 2)
+                                    for r in rows})
     for kind in (BenchKind.PutLatency, BenchKind.GetLatency):
         rows = run_p2p(rt, BenchSpec(kind, (8,), iters=200, warmup=20, transfer=TransferKind.D2D))
         res[kind.value] = {r.size_bytes: round(r.mean_us, 2) for r in rows}
@@ -689,10 +716,13 @@ def measure_collectives(rt: Runtime, sizes=(64 * MIB, 1 << 30), iters: int = 5) 
     comm = coll.bootstrap(rt, rt.world)
     k = rt.nranks
     for kind in (BenchKind.Allreduce, BenchKind.Bcast):
-        rows = run_collective(rt, BenchSpec(kind, tuple(sizes), iters=iters, warmup=2), comm)
         f = 2 * (k - 1) / k if kind is BenchKind.Allreduce else 1.0
-        out[kind.value] = {r.size_bytes: round(f * r.size_bytes / r.mean_us / 1e3, 2)
-                           for r in rows}
+        out[kind.value] = {}
+        for size in sizes:
+            rows = run_collective(rt, BenchSpec(kind, (size,), iters=bw_iters(size, iters),
+                                                warmup=2), comm)
+            out[kind.value].update({r.size_bytes: round(f * r.size_bytes / r.mean_us / 1e3, 2)
+                                    for r in rows})
     if rt.rank != 0:
         return None
     return {"workload": f"collectives_k{k}", "unit": "GB/s (busBW)",
