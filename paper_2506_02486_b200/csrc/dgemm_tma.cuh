@@ -124,6 +124,12 @@ __global__ void __launch_bounds__(SH::THREADS, SH::MINB)
     constexpr int WM = SH::WM, WN = SH::WN;
     constexpr int STAGE_BYTES = SH::STAGE_BYTES;
     extern __shared__ uint8_t raw[];
+    // 1024-byte aligned for the 128-byte swizzle.  The cast through uintptr_t
+    // makes the fragment reads generic LD.E; keeping the pointer in the shared
+    // window (LDS, 223 instead of 254 registers) measured slower -- the
+    // compiler then issues each k-step's fragment loads just before their
+    // DMMAs: 8192^3 34.3 -> 32.4 TFLOP/s, DMMA pipe 93.4 -> 88.4 %
+    // (profiles/r02_dgemm_lds_variant.txt)
     uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
     uint64_t *full = (uint64_t *)(sm + (size_t)STAGES * STAGE_BYTES);
     uint64_t *empty = full + STAGES;
