@@ -13,10 +13,22 @@ if [[ $SKIP != *tests* ]]; then
 fi
 if [[ $SKIP != *bench* ]]; then
   timeout 900 python bench.py > $O/bench_n1.jsonl 2> $O/bench_n1.err
-  if [ $NGPU -ge 2 ]; then
-    timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NGPU --master-addr 127.0.0.1 \
-      --master-port 29531 bench.py --gpus $NGPU > $O/bench_n$NGPU.jsonl 2> $O/bench_n$NGPU.err
-  fi
+  for n in 2 4; do
+    [ $NGPU -ge $n ] || continue
+    timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+      --master-port 2953$n bench.py --gpus $n > $O/bench_n$n.jsonl 2> $O/bench_n$n.err
+  done
+  timeout 900 python bench.py --impl reference > $O/reference_n1.jsonl 2> $O/reference_n1.err
+fi
+if [[ $SKIP != *coll* ]] && [ $NGPU -ge 2 ]; then
+  g++ -O2 -std=c++20 tools/coll_probe.cpp -o tools/coll_probe.bin paper_2506_02486_b200/libdiomp_b200.so \
+    -Wl,-rpath,'$ORIGIN/../paper_2506_02486_b200' > $O/coll_build.log 2>&1
+  for k in 2 4; do
+    [ $NGPU -ge $k ] || continue
+    for op in allreduce bcast; do timeout 300 ./tools/coll_probe.bin $op $k > $O/collprobe_${op}_k$k.txt 2>&1; done
+  done
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+    --master-port 29539 bench.py --gpus 2 --workload p2p --steps 20 > $O/p2p_n2.jsonl 2> $O/p2p_n2.err
 fi
 if [[ $SKIP != *ncu* ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
