@@ -7,7 +7,9 @@
 * tests/c/rma_abi.c -- a C program that reaches the global address space
   through the rank-addressed RMA context (peer table, put/get -> op,
   op_query/op_wait, fence_group), compiled with gcc against
-  include/diomp_b200.h and libdiomp_b200.so.
+  include/diomp_b200.h and libdiomp_b200.so;
+* tests/c/coll_abi.c -- two host threads driving the collectives (allreduce,
+  bcast, the LL path through diomp_ll_call) on two GPUs from C.
 """
 
 import importlib.util
@@ -17,7 +19,7 @@ import subprocess
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, NGPU, ROOT
+from conftest import GOLDEN, NGPU, ROOT, need_gpus
 
 pytestmark = pytest.mark.gpu
 
@@ -61,5 +63,18 @@ def test_c_caller_reaches_global_memory_through_the_rma_context(tmp_path):
                            "-L", libdir, "-l:libdiomp_b200.so", f"-Wl,-rpath,{libdir}"])
     gpus = ["0", "1"] if NGPU >= 2 else ["0", "0"]
     out = subprocess.run([str(exe), *gpus], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "all ok" in out.stdout
+
+
+@need_gpus(2)
+def test_c_caller_drives_collectives(tmp_path):
+    exe = tmp_path / "coll_abi"
+    libdir = os.path.join(ROOT, "paper_2506_02486_b200")
+    subprocess.check_call(["gcc", "-O2", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "c", "coll_abi.c"), "-o", str(exe),
+                           "-L", libdir, "-l:libdiomp_b200.so", "-lpthread",
+                           f"-Wl,-rpath,{libdir}"])
+    out = subprocess.run([str(exe), "0", "1"], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "all ok" in out.stdout
