@@ -73,7 +73,9 @@ def stencil(g=512, nx=None):
     shape = (nx + 8, g + 8, g + 8)
     a = torch.rand(shape, dtype=torch.float64, device="cuda")
     b = torch.rand(shape, dtype=torch.float64, device="cuda")
-    ms = _time(lambda: kernels.stencil_update(b, a, b, 3 * w[0], w, w, w, 4), iters=10)
+    iters = int(os.environ.get("PROBE_ITERS", "10"))
+    ms = _time(lambda: kernels.stencil_update(b, a, b, 3 * w[0], w, w, w, 4), iters=iters,
+               warm=max(3, iters // 10))
     pts = nx * g * g
     return {"probe": "stencil_update", "grid": [nx, g, g], "ms": ms, "gpts": pts / ms / 1e6,
             "GBps_24B": 24 * pts / ms / 1e6}
