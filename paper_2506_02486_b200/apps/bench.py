@@ -566,6 +566,17 @@ def measure_stencil_config1(rt: Runtime, n: int = 128, steps: int = 100) -> dict
     spec = StencilSpec(n, n, n, steps=steps)
     runner = StencilRunner(rt, spec)
     timer = _Timer(rt)
+    # one untimed warm-up run (the first run pays the module / tensor-map /
+    # launch-path warm-up), then zero fields again for the checksummed run
+    runner.enqueue(steps) if runner.mode == "fused" else runner.run(steps)
+    runner.stream.synchronize()
+    rt.barrier(rt.world)   # every neighbour's last halo stores into our ghost planes landed
+    base = rt.gm.base(0)
+    for rec in (runner.field_a, runner.field_b):
+        _native.call("diomp_memset_async", base + rec.addr.offset, 0, runner.nbytes,
+                     runner.stream.handle)
+    runner.stream.synchronize()
+    runner.step = 0
     rt.barrier(rt.world)
     timer.stream = runner.stream.handle
     timer.start()
