@@ -203,7 +203,13 @@ def _advance(comm: Communicator, n: int, channel: int = CHANNEL_COLL):
 
 
 # ---- one-shot low-latency (LL) path for small messages ---------------------
-LL_MAX_BYTES = int(os.environ.get("DIOMP_LL_MAX", str(32 * 1024)))
+# Up to the slot capacity (half an LL slot: payload words travel with their
+# flags) -- measured faster than the handshake path at every size that fits
+# (2 B200, f32 allreduce, blocking: 1 KiB 21.3 vs 37.2 us, 128 KiB 23.7 vs
+# 34.5 us; back to back 10.4 vs 11.8 us at 128 KiB; profiles/r02_ll_crossover.txt).
+# The slot is 2*chunk/(2*endpoints) of the reference-sized scratch, so the
+# ceiling is ~255 KiB at 2 endpoints, ~127 KiB at 4, ~63 KiB at 8.
+LL_MAX_BYTES = int(os.environ.get("DIOMP_LL_MAX", str(1 << 20)))
 
 
 def _ll_slot_bytes(comm: Communicator) -> int:
