@@ -213,7 +213,11 @@ int diomp_allreduce(const diomp_team *team, uint64_t send_off, uint64_t recv_off
  * stores to every non-root.  epoch_to[q] / epoch_from[q] = this call's epoch
  * for the pair (both ends count every LL call between them, from 1); the
  * LL region is `ll_off` in every member's segment, slot_bytes per (source
- * endpoint, parity), at least 2x the payload.                               */
+ * endpoint, parity), at least 2x the payload.  The 4 KiB below `ll_off`
+ * (zero at start) hold the acknowledgement bank: a consumer acknowledges
+ * each call to its writers, and a writer reuses a parity slot only after the
+ * peer acknowledged the call that used it last (so a bcast root, which gets
+ * no words back, can never overwrite a slot a slow peer has not read).      */
 typedef struct {
     int32_t k, pos, device, dtype, op, root, mode;  /* mode 0 allreduce, 1 bcast (bytes) */
     int32_t _pad;

@@ -613,6 +613,50 @@ __device__ __forceinline__ uint64_t *ll_slot(const LLArgs &a, int at, int from, 
     return (uint64_t *)(a.base[at] + a.ll_off + ((uint64_t)a.slot[from] * 2 + (epoch & 1)) * a.slot_bytes);
 }
 
+// Acknowledgements.  The two-parity reuse argument above needs return
+// traffic: a bcast root receives nothing from its peers, so on its own it
+// could run two calls ahead and overwrite a parity slot a slow peer has not
+// read yet (the peer then waits forever for an epoch that was overwritten).
+// So every member acknowledges every call to every peer of the team: once
+// all its CTAs are done with call e (read what it had to read), the last CTA
+// stores e into each peer's ack bank -- also where nothing travelled between
+// the two (a bcast between two non-roots, the root's side of a bcast),
+// because both ends count every LL call on the pair.  A writer stores call e
+// into a peer's parity slot only after the peer acknowledged call e-2, the
+// previous call of that parity -- a local poll, normally satisfied at once.
+// Bank: the 4 KiB below ll_off in every member's segment, ack[source
+// endpoint] (u64), then a u32 last-CTA counter.
+constexpr uint64_t LL_ACK_BELOW = 4096;
+
+__device__ __forceinline__ uint64_t *ll_ack(const LLArgs &a, int at, int from) {
+    return (uint64_t *)(a.base[at] + a.ll_off - LL_ACK_BELOW) + a.slot[from];
+}
+
+__device__ __forceinline__ unsigned int *ll_counter(const LLArgs &a) {
+    return (unsigned int *)(a.base[a.pos] + a.ll_off - LL_ACK_BELOW + 8 * DIOMP_MAX_TEAM);
+}
+
+// before writing this call's words into q's slot: q consumed call e-2
+__device__ __forceinline__ void ll_wait_ack(const LLArgs &a, int q) {
+    const uint32_t e = a.ep_to[q];
+    if (e > 2) wait_ge(ll_ack(a, a.pos, q), (uint64_t)(e - 2));
+}
+
+// after every CTA is done with this call: the last CTA acknowledges it to
+// every peer
+__device__ __forceinline__ void ll_send_acks(const LLArgs &a) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ll_counter(a), 1u) == gridDim.x - 1) {
+            atomicExch(ll_counter(a), 0u);
+            __threadfence_system();
+            for (int q = 0; q < a.k; ++q)
+                if (q != a.pos) st_release_sys(ll_ack(a, q, a.pos), (uint64_t)a.ep_from[q]);
+        }
+    }
+}
+
 __device__ __forceinline__ uint32_t ll_wait(const uint64_t *p, uint32_t epoch) {
     uint64_t v;
     const uint64_t t0 = globaltimer_ns();
@@ -640,6 +684,8 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
     const uint64_t gsz = (uint64_t)gridDim.x * blockDim.x;
     const T *send = (const T *)(a.base[me] + a.send_off);
     T *recv = (T *)(a.base[me] + a.recv_off);
+    if (threadIdx.x < k && threadIdx.x != me) ll_wait_ack(a, threadIdx.x);
+    __syncthreads();
     // push my vector into every peer's slot
     for (uint64_t e = gtid; e < n; e += gsz) {
         uint32_t w[W];
@@ -681,6 +727,7 @@ __global__ void __launch_bounds__(256) ll_allreduce_kernel(const __grid_constant
         }
         recv[e] = acc;
     }
+    ll_send_acks(a);
 }
 
 // bcast of `count` bytes at send_off: the root stores 4-byte words (zero-padded
@@ -692,6 +739,8 @@ __global__ void __launch_bounds__(256) ll_bcast_kernel(const __grid_constant__ L
     const uint64_t gsz = (uint64_t)gridDim.x * blockDim.x;
     uint8_t *buf = (uint8_t *)(a.base[me] + a.send_off);
     if (me == root) {
+        if (threadIdx.x < k && threadIdx.x != root) ll_wait_ack(a, threadIdx.x);
+        __syncthreads();
         for (uint64_t i = gtid; i < nw; i += gsz) {
             uint32_t w = 0;
             const uint64_t o = i * 4;
@@ -699,14 +748,15 @@ __global__ void __launch_bounds__(256) ll_bcast_kernel(const __grid_constant__ L
             for (int q = 0; q < k; ++q)
                 if (q != root) ll_store(ll_slot(a, q, root, a.ep_to[q]) + i, a.ep_to[q], w);
         }
-        return;
+    } else {
+        const uint64_t *src = ll_slot(a, me, root, a.ep_from[root]);
+        for (uint64_t i = gtid; i < nw; i += gsz) {
+            const uint32_t w = ll_wait(src + i, a.ep_from[root]);
+            const uint64_t o = i * 4;
+            for (int b = 0; b < 4 && o + b < a.count; ++b) buf[o + b] = (uint8_t)(w >> (8 * b));
+        }
     }
-    const uint64_t *src = ll_slot(a, me, root, a.ep_from[root]);
-    for (uint64_t i = gtid; i < nw; i += gsz) {
-        const uint32_t w = ll_wait(src + i, a.ep_from[root]);
-        const uint64_t o = i * 4;
-        for (int b = 0; b < 4 && o + b < a.count; ++b) buf[o + b] = (uint8_t)(w >> (8 * b));
-    }
+    ll_send_acks(a);
 }
 
 template <typename T, typename OP>

@@ -146,6 +146,44 @@ def test_device_flag_mode_back_to_back():
         assert all(r[rep] == want for r in res)
 
 
+@need_gpus(2)
+def test_ll_bcast_root_never_overruns_a_slow_peer():
+    """A bcast root gets no words back from its peers, so without the
+    acknowledgement bank it could run two LL calls ahead and overwrite a
+    parity slot a slow peer has not read yet (the peer would then wait on an
+    epoch that no longer exists).  Rank 1 dawdles on the host between calls
+    while rank 0 issues blocking small bcasts back to back; every payload
+    must arrive intact, interleaved with LL allreduces."""
+    import time
+
+    from paper_2506_02486_b200 import collectives as coll
+    from paper_2506_02486_b200.emulate import run_emulated
+    op = coll.ReduceOp(coll.ReduceKind.Sum, coll.ElementType.i32)
+
+    def fn(rt):
+        comm = coll.bootstrap(rt, rt.world)
+        assert comm.device_sync
+        buf = rt.alloc_symmetric(64 * 1024, 0)
+        acc = rt.alloc_symmetric(4096, 0)
+        rng = np.random.default_rng(31)
+        bad = 0
+        for i in range(150):
+            size = int(rng.integers(1, 40000))
+            if rt.rank == 0:
+                rt.gm.view(0, buf.addr.offset, size)[:] = bytes([(i * 7 + j) & 255 for j in range(64)]) * (size // 64) + bytes((i * 7 + j) & 255 for j in range(size % 64))
+            elif i % 3 == 0:
+                time.sleep(0.002)   # the peer falls behind the root
+            coll.bcast(comm, buf.addr, size, root=0)
+            want = bytes([(i * 7 + j) & 255 for j in range(64)]) * (size // 64) + bytes((i * 7 + j) & 255 for j in range(size % 64))
+            if bytes(rt.gm.view(0, buf.addr.offset, size)) != want:
+                bad += 1
+            if i % 10 == 9:
+                coll.allreduce(comm, acc.addr, acc.addr, 100, op)
+        return bad
+
+    assert run_emulated(2, fn, segment_bytes=16 * MIB) == [0, 0]
+
+
 _EXPERIMENTS = pytest.mark.skipif(
     not __import__("paper_2506_02486_b200._native", fromlist=["x"]).has_experiments(),
     reason="experiments build only (-DDIOMP_EXPERIMENTS)")
