@@ -893,16 +893,14 @@ int diomp_ll_call(void *ctx, diomp_ll_args *x, void *stream, void *after, int32_
     cudaStream_t s = (cudaStream_t)stream;
     DIOMP_CUDA_TRY(cudaSetDevice(x->device));
     if (after && after != stream) {
-        cudaEvent_t ev;
-        {
-            std::lock_guard<std::mutex> lk(c->mu);
-            if ((int)c->order_ev.size() <= x->device) c->order_ev.resize(x->device + 1, nullptr);
-            if (!c->order_ev[x->device])
-                DIOMP_CUDA_TRY(cudaEventCreateWithFlags(&c->order_ev[x->device], cudaEventDisableTiming));
-            ev = c->order_ev[x->device];
-        }
-        // record + wait back to back on this thread: a later record on the
-        // same event cannot slip in between for this caller's ordering
+        // record + wait under the lock: another thread's record on the same
+        // event cannot slip in between and order this call after the wrong
+        // stream
+        std::lock_guard<std::mutex> lk(c->mu);
+        if ((int)c->order_ev.size() <= x->device) c->order_ev.resize(x->device + 1, nullptr);
+        if (!c->order_ev[x->device])
+            DIOMP_CUDA_TRY(cudaEventCreateWithFlags(&c->order_ev[x->device], cudaEventDisableTiming));
+        cudaEvent_t ev = c->order_ev[x->device];
         DIOMP_CUDA_TRY(cudaEventRecord(ev, (cudaStream_t)after));
         DIOMP_CUDA_TRY(cudaStreamWaitEvent(s, ev, 0));
     }
