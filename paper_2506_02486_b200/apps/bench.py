@@ -469,6 +469,9 @@ def _dgemm_cli(args):
     got = rt.ctrl.allgather(tuple(range(rt.nranks)), "gemmbench", pickle.dumps(min(ms)))
     t = max(pickle.loads(b) for _, b in got) / 1e3
     ring.release()
+    ring = CannonRing(rt, spec, device_seed=0)
+    e2e = _ring_e2e(rt, ring, n)
+    ring.release()
     # library reference point: cuBLAS DGEMM (torch addmm, f64) over the same
     # per-endpoint shapes -- P products C(ns x n) += A(ns x ns) @ B(ns x n) --
     # without the stripe shift
@@ -487,6 +490,7 @@ def _dgemm_cli(args):
                               "unit": "TFLOP/s per GPU",
                               "frac": round(t_cublas / t, 4),
                               "peak_source": "cuBLAS DGEMM on the same shapes, this run"}}
+        extra["e2e"] = e2e
         if rt.nranks == 1 and os.environ.get("BENCH_GEMM_CPU", "1") != "0":
             extra["cpu_baseline"] = _cpu_dgemm_sample(n)
         _line(rt, "dgemm_ring_tflops", round(tflops, 3), "TFLOP/s", args,
@@ -614,6 +618,36 @@ def measure_stencil_config1(rt: Runtime, n: int = 128, steps: int = 100) -> dict
                     "d2h_bytes": runner.nbytes * rt.nranks}}
 
 
+def _ring_e2e(rt: Runtime, ring, n: int) -> dict:
+    """End to end on a fresh ring (step 0): every rank copies its A stripe and
+    its B stripe from pinned host buffers, the ring multiplies, every rank
+    copies its C stripe back; wall clock, max over ranks."""
+    import torch
+    spec = ring.spec
+    (e, st), = ring.local.items()
+    g = torch.Generator().manual_seed(4000 + e)
+    ha = (torch.rand(spec.ns, n, dtype=torch.float64, generator=g) * 2 - 1).pin_memory()
+    hb = (torch.rand(spec.ns, n, dtype=torch.float64, generator=g) * 2 - 1).pin_memory()
+    hc = torch.empty(spec.ns, n, dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    rt.barrier(rt.world)
+    t0 = time.perf_counter()
+    st["a"].copy_(ha, non_blocking=True)
+    ring.stripe(st["dev"], 0).copy_(hb, non_blocking=True)
+    st["c"].zero_()
+    torch.cuda.synchronize()
+    for _ in range(spec.p):
+        ring.enqueue_step() if ring.sync else ring.run()
+    ring.synchronize()
+    hc.copy_(st["c"], non_blocking=True)
+    torch.cuda.synchronize()
+    sec = _max_over_ranks(rt, "gemm/e2e", time.perf_counter() - t0)
+    nb = spec.ns * n * 8 * spec.p
+    return {"value": round(2.0 * n ** 3 / sec / 1e12, 3), "unit": "TFLOP/s", "seconds": round(sec, 4),
+            "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": nb,
+            "note": "A and B stripes H2D from pinned host memory, the ring, C stripes D2H, every rank"}
+
+
 def measure_dgemm_ring(rt: Runtime, n: int = 16384, reps: int = 3, host_check: bool = True):
     """BASELINE configs[3]: the n x n fp64 ring multiply on this job's
     endpoints.  Device time per multiply (best of `reps`, max over ranks), the
@@ -665,6 +699,8 @@ def measure_dgemm_ring(rt: Runtime, n: int = 16384, reps: int = 3, host_check: b
                       "seconds": round(e2e_s, 4), "h2d_bytes": 2 * n * n * 8,
                       "d2h_bytes": n * n * 8}
         del pa, pb, pc, got, want
+    elif spec.p > 1:
+        out["e2e"] = _ring_e2e(rt, ring, n)
     ms = []
     rt.barrier(rt.world)
     for _ in range(reps):
