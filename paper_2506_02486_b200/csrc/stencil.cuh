@@ -187,7 +187,7 @@ __device__ __forceinline__ void store4(double *b, int64_t NZ, const double (&o)[
 // neighbour rows live (rows -t / 1+t of tap t are rows 1-(t+1) / (t+1) of
 // tap t+1).  The slot of plane q-R is released (empty barrier) after its
 // last use here.
-template <int J, bool FULL>
+template <int J, bool FULL, bool HALO>
 __device__ __forceinline__ void step_plane(const Params &p, const double *sm, uint64_t *full,
                                            uint64_t *empty, const double *psm, uint64_t *pfull,
                                            uint64_t *pempty, double (&Q)[9][4], Lane &ln, int q,
@@ -266,12 +266,14 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
                 if (pt == ln.src_pt) out[pt] = __dadd_rn(out[pt], p.amp);
         }
         store4<FULL>(ln.pn, p.NZ, out, ln);
-        if (ln.pl && ln.x < 2 * R) store4<FULL>(ln.pl, p.NZ, out, ln);
-        if (ln.pr && ln.x >= p.nxl) store4<FULL>(ln.pr, p.NZ, out, ln);
         const int64_t pstride = p.NY * p.NZ;
+        if (HALO) {
+            if (ln.pl && ln.x < 2 * R) store4<FULL>(ln.pl, p.NZ, out, ln);
+            if (ln.pr && ln.x >= p.nxl) store4<FULL>(ln.pr, p.NZ, out, ln);
+            if (ln.pl) ln.pl += pstride;
+            if (ln.pr) ln.pr += pstride;
+        }
         ln.pn += pstride;
-        if (ln.pl) ln.pl += pstride;
-        if (ln.pr) ln.pr += pstride;
         ln.x += 1;
     }
     if (q >= R) {  // plane q-R had its last read (centre of this output plane)
@@ -284,7 +286,7 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
     }
 }
 
-template <bool FULL>
+template <bool FULL, bool HALO>
 __device__ __forceinline__ void consume(const Params &p, const double *sm, uint64_t *full,
                                        uint64_t *empty, const double *psm, uint64_t *pfull,
                                        uint64_t *pempty, Lane &ln, int L) {
@@ -297,7 +299,7 @@ __device__ __forceinline__ void consume(const Params &p, const double *sm, uint6
     uint32_t ph = 0;
 #define DIOMP_STEP(JJ) \
     if (q + JJ < L) \
-        step_plane<JJ, FULL>(p, sm, full, empty, psm, pfull, pempty, Q, ln, q + JJ, L, s, ph);
+        step_plane<JJ, FULL, HALO>(p, sm, full, empty, psm, pfull, pempty, Q, ln, q + JJ, L, s, ph);
     for (int q = 0; q < L; q += 9) {
         DIOMP_STEP(0) DIOMP_STEP(1) DIOMP_STEP(2) DIOMP_STEP(3) DIOMP_STEP(4)
         DIOMP_STEP(5) DIOMP_STEP(6) DIOMP_STEP(7) DIOMP_STEP(8)
@@ -305,6 +307,11 @@ __device__ __forceinline__ void consume(const Params &p, const double *sm, uint6
 #undef DIOMP_STEP
 }
 
+// HALO: the kernel carries the epilogue stores into the neighbours' ghost
+// planes.  Launches without neighbours use the instantiation without them:
+// merely having those (never executed) stores in the loop body costs 2 %
+// (profiles/r02_stencil_halo_codegen.txt).
+template <bool HALO>
 __global__ void __launch_bounds__(THREADS, 1)
     stencil_tma_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap pmap,
                        const __grid_constant__ Params p) {
@@ -411,8 +418,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int64_t dy = p.src_y - y, dz = p.src_z - z;
             if (dy >= 0 && dy < 2 && dz >= 0 && dz < 2) ln.src_pt = (int)(dy * 2 + dz);
         }
-        if (ln.full) consume<true>(p, sm, full, empty, psm, pfull, pempty, ln, L);
-        else consume<false>(p, sm, full, empty, psm, pfull, pempty, ln, L);
+        if (ln.full) consume<true, HALO>(p, sm, full, empty, psm, pfull, pempty, ln, L);
+        else consume<false, HALO>(p, sm, full, empty, psm, pfull, pempty, ln, L);
     }
 
 }
@@ -581,7 +588,10 @@ static int launch_fast(const CUtensorMap &map, const CUtensorMap &pmap, Params &
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_set[dev]) {
-        DIOMP_CUDA_TRY(cudaFuncSetAttribute(stencil_tma_kernel,
+        DIOMP_CUDA_TRY(cudaFuncSetAttribute(stencil_tma_kernel<true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SMEM_BYTES));
+        DIOMP_CUDA_TRY(cudaFuncSetAttribute(stencil_tma_kernel<false>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)SMEM_BYTES));
         attr_set[dev] = true;
@@ -614,7 +624,10 @@ static int launch_fast(const CUtensorMap &map, const CUtensorMap &pmap, Params &
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    DIOMP_CUDA_TRY(cudaLaunchKernelEx(&cfg, stencil_tma_kernel, map, pmap, p));
+    if (p.left_next || p.right_next)
+        DIOMP_CUDA_TRY(cudaLaunchKernelEx(&cfg, stencil_tma_kernel<true>, map, pmap, p));
+    else
+        DIOMP_CUDA_TRY(cudaLaunchKernelEx(&cfg, stencil_tma_kernel<false>, map, pmap, p));
     return DIOMP_OK;
 }
 
