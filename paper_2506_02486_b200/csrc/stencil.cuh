@@ -22,10 +22,13 @@
 //     plane's slot with 16 B shared loads (conflict-free rows), interleaved
 //     tap by tap so only a sliding pair of rows is live;
 //   * u_next is stored with 16 B coalesced stores.
-// Measured (1024^3, one B200): 258.6 Gpts/s = 0.947 of the measured HBM copy
-// peak at 24 B/point.  Round 1's 24 x 64 tiles (576-byte TMA rows, 12 compute
-// warps) ran 243-246: the longer rows and the two extra compute warps are
-// each worth about half of the gain (profiles/r02_stencil_shapes.txt).
+// Measured (1024^3, one B200): 262.5 Gpts/s = 0.962 of the measured HBM copy
+// peak at 24 B/point, DRAM traffic 1.024x the minimum.  Round 1's 24 x 64
+// tiles (576-byte TMA rows, 12 compute warps) ran 243-246: the longer rows
+// and the two extra compute warps are each worth about half of the gain to
+// 258.6 (profiles/r02_stencil_shapes.txt); the instantiation without the halo
+// epilogue for launches without neighbours the rest
+// (profiles/r02_stencil_halo_codegen.txt).
 // Fused driver epilogue: output planes [R,2R) / [nxl, nxl+R) are also stored
 // into the left / right neighbour's u_next ghost planes over NVLink (peer
 // pointers), the point source is added in-register (one extra rounded add,
