@@ -162,8 +162,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // Per-thread streaming state (pointers advance by one plane per output plane).
 struct Lane {
     double *pn;         // u_next at (x, y, z) of the thread's first point
-    double *pl;         // left neighbour's ghost copy of pn (or null)
-    double *pr;         // right neighbour's ghost copy of pn (or null)
     int64_t x;          // current output plane (full-array index)
     int so;             // slot offset (doubles) of the thread's first point
     int src_pt;         // which of the 4 points is the source (y/z match), -1: none
@@ -271,10 +269,13 @@ __device__ __forceinline__ void step_plane(const Params &p, const double *sm, ui
         store4<FULL>(ln.pn, p.NZ, out, ln);
         const int64_t pstride = p.NY * p.NZ;
         if (HALO) {
-            if (ln.pl && ln.x < 2 * R) store4<FULL>(ln.pl, p.NZ, out, ln);
-            if (ln.pr && ln.x >= p.nxl) store4<FULL>(ln.pr, p.NZ, out, ln);
-            if (ln.pl) ln.pl += pstride;
-            if (ln.pr) ln.pr += pstride;
+            // pn's copies in the neighbours' ghost planes, from the parameters
+            // (no per-plane pointer bookkeeping in the loop: N=2 512 -> 517,
+            // N=4 988 -> 994 Gpts/s, profiles/r02_stencil_halo_codegen.txt)
+            if (ln.x < 2 * R && p.left_next)
+                store4<FULL>(p.left_next + p.nxl * pstride + (ln.pn - p.u_next), p.NZ, out, ln);
+            if (ln.x >= p.nxl && p.right_next)
+                store4<FULL>(p.right_next - p.nxl * pstride + (ln.pn - p.u_next), p.NZ, out, ln);
         }
         ln.pn += pstride;
         ln.x += 1;
@@ -413,8 +414,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         ln.so = (R + ry) * BZ + R + zz;
         const int64_t g0 = (xa * p.NY + y) * p.NZ + z;
         ln.pn = p.u_next + g0;
-        ln.pl = p.left_next ? p.left_next + p.nxl * p.NY * p.NZ + g0 : nullptr;
-        ln.pr = p.right_next ? p.right_next - p.nxl * p.NY * p.NZ + g0 : nullptr;
         ln.x = xa;
         ln.src_pt = -1;
         if (p.src_x >= xa && p.src_x < xb) {
