@@ -591,10 +591,10 @@ static bool team_ok(const diomp_team *t) {
 //     order (block b = [b*count/k, (b+1)*count/k) folded from position b), so
 //     each position computes the full result itself -- bit-identical.
 //   bcast: the root stores into every non-root's slot; non-roots copy out.
-// Slots: per source endpoint, two parities (epoch & 1).  Writing call n+2's
-// parity into a peer's slot is safe without a handshake: this position's call
-// n+1 received the peer's call n+1 words, so the peer's stream had finished
-// call n -- the last reader of that parity.  Epochs are per pair (both ends
+// Slots: per source endpoint, two parities (epoch & 1); a parity is reused
+// only after the peer acknowledged the call that used it last (the
+// acknowledgement bank below -- receiving a peer's words alone does not
+// prove it: a bcast root receives none).  Epochs are per pair (both ends
 // count every LL call between them), flags start at 0 (segments are
 // zero-filled), epochs at 1.
 // ---------------------------------------------------------------------------
